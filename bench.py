@@ -1,0 +1,407 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 page-cipher engine (BASELINE.json metric: GB/s of
+4 KiB pages en/decrypted).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--rounds R] [--pages P]
+    python bench.py --impl reference ...      # the reference CPU path
+
+Workload (BASELINE.json configs[1]): a 1 GiB batch (262,144 pages) of random
+4 KiB pages resident in HBM, ChaCha20, contiguous vaddrs from BASE_VADDR
+(pkg/src/pagecrypt/client.py:42), pid 1.  One step = one pass of the hot path
+over the batch = one crypt_pages() call = one kernel launch.  At N GPUs each
+rank owns its own 1 GiB page range (weak scaling, no collective on the data
+path); the only cross-rank traffic is the barrier and the max-over-ranks time.
+
+value    device-resident GB/s (CUDA events on the launching stream, inputs
+         already in HBM, 1 GiB > 126 MB L2 so no flush is needed)
+e2e      the same metric through the public host API (pinned host pages; the
+         H2D copy, cipher and D2H copy of every page are inside the timed region)
+roofline the crypt kernel against min(int32 roof for the ARX op count, HBM
+         roof for 8 B/page-byte), both measured on this GPU in this run
+cpu_baseline  the oracle port (oracle/liboracle.so, scalar C, one page per call
+         like cipher.crypt_page) on all host cores, rank 0 at N=1, bounded sample
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE_VADDR = 0x1_0000_0000
+PAGE = 4096
+METRIC = "GB/s of pages en/decrypted (device-resident and host-resident) at 1/2/4/8 B200"
+
+
+def ops_per_page(rounds: int) -> int:
+    """Op-count convention: 12 int32 ops per quarter round,
+    4*R quarter rounds per block, + 16 feed-forward adds + 16 data XORs."""
+    return 64 * (48 * rounds + 32)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.25)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2])); pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "power_w_max": max(pw), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port; the reference itself is Python and does not travel)
+
+
+def cpu_port_rate(rounds: int, target_s: float, threads: int, pages_per_batch: int = 4096) -> dict:
+    """Time the oracle port (scalar C, one page per call as cipher.crypt_page)
+    on `threads` host threads over batches of the bench workload."""
+    from oracle import coracle
+
+    rng = np.random.default_rng(1)
+    pages = rng.integers(0, 256, size=(pages_per_batch, PAGE), dtype=np.uint8)
+    out = np.empty_like(pages)
+    key = np.random.default_rng(0).bytes(32)
+    coracle.crypt_pages(key, None, None, pages[:64], rounds=rounds, vaddr0=BASE_VADDR, pid0=1)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        coracle.crypt_pages(key, None, None, pages, rounds=rounds, nthreads=threads, out=out,
+                            vaddr0=BASE_VADDR + PAGE * done, pid0=1)
+        done += pages_per_batch
+        el = time.perf_counter() - t0
+        if el >= target_s:
+            break
+    return {"value": done * PAGE / el / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{done} pages ({done * PAGE / 2**20:.0f} MiB) of the bench workload "
+                      f"(ChaCha{rounds}, contiguous vaddrs, pid 1) in {el:.1f} s on {threads} host "
+                      f"threads; oracle/chacha_oracle.c, one page per call like cipher.crypt_page",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference's CPU path on the box's host cores.
+    The reference package cannot travel to the GPU box, so this runs the oracle
+    port of it (the tier's stated fallback), all host threads, rank 0 only."""
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    from oracle import coracle
+
+    n_sample = args.ref_pages
+    rng = np.random.default_rng(1)
+    pages = rng.integers(0, 256, size=(n_sample, PAGE), dtype=np.uint8)
+    out = np.empty_like(pages)
+    key = np.random.default_rng(0).bytes(32)
+    for _ in range(args.warmup):
+        coracle.crypt_pages(key, None, None, pages, rounds=args.rounds, nthreads=threads, out=out,
+                            vaddr0=BASE_VADDR, pid0=1)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        coracle.crypt_pages(key, None, None, pages, rounds=args.rounds, nthreads=threads, out=out,
+                            vaddr0=BASE_VADDR + PAGE * n_sample * i, pid0=1)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.steps * n_sample * PAGE / total / 1e9
+    sample = (f"each step {n_sample} pages ({n_sample * PAGE / 2**20:.0f} MiB) of the "
+              f"{args.pages}-page workload, ChaCha{args.rounds}, {threads} host threads, "
+              "oracle/chacha_oracle.c (port of cipher.crypt_page; the Python reference does not travel)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample, "cpu": _cpu_model()},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world: int) -> dict:
+    return {"workload": f"{args.pages * PAGE / 2**30:g} GiB device-resident batch of 4 KiB pages per GPU, "
+                        f"ChaCha{args.rounds} (BASELINE configs[1])",
+            "pages_per_gpu": args.pages, "rounds": args.rounds, "vaddrs": "contiguous from 0x100000000",
+            "pid": 1, "parallelism": f"page-range x{world} (no collective)",
+            "l2": "inputs (1 GiB) larger than the 126 MB L2; no flush"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--rounds", type=int, default=20, choices=(8, 12, 20))
+    ap.add_argument("--pages", type=int, default=262_144, help="pages per GPU (default 1 GiB)")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--ref-pages", type=int, default=8192, help="reference arm: pages per step")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip rounds 8/12 + latency sweeps")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_09252_b200 as pc
+    from paper_2004_09252_b200 import _native
+    from paper_2004_09252_b200.partition import max_over_ranks
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    n = args.pages
+    # this rank's page range: disjoint vaddrs per rank (partition.shard of world*n)
+    vaddr0 = BASE_VADDR + PAGE * n * rank
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+    pages = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8, device=dev, generator=g)
+    out = torch.empty_like(pages)
+    key = pc.DeviceKey.generate(local_rank)  # production key path: never in host RAM
+    stream = torch.cuda.current_stream(dev)
+
+    def step(rounds):
+        pc.crypt_pages(key, vaddr0, 1, pages, out=out, rounds=rounds, stream=stream, check=False)
+
+    def timed(rounds, steps, warmup):
+        for _ in range(warmup):
+            step(rounds)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step(rounds)
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        return e0.elapsed_time(e1)  # ms on the launching stream
+
+    # integer roofline denominators, measured on this GPU now
+    peaks = {}
+    for kind, name in ((0, "lop3"), (1, "iadd3"), (2, "imad"), (3, "shf"), (4, "arx_mix")):
+        v = _native.ctypes.c_double()
+        _native.call("pc_intpeak", local_rank, kind, _native.ctypes.byref(v))
+        peaks[name] = v.value
+
+    with ClockSampler(local_rank) as clk:
+        total_ms = timed(args.rounds, args.steps, args.warmup)
+    t_max = max_over_ranks(total_ms, device=dev)
+    bytes_per_step = n * PAGE
+    value = world * bytes_per_step * args.steps / (t_max / 1e3) / 1e9
+    kernel_ms = total_ms / args.steps  # one launch per step
+
+    def roofline(rounds, k_ms):
+        achieved = bytes_per_step / (k_ms / 1e3) / 1e9  # page GB/s of one launch
+        opb = ops_per_page(rounds) / PAGE
+        int_roof = peaks["arx_mix"] / opb / 1e9
+        hbm_peak, hbm_src = _hbm_peak()
+        hbm_roof = hbm_peak / 2.0  # each page byte is read once and written once
+        bound = "int32" if int_roof < hbm_roof else "hbm"
+        peak = min(int_roof, hbm_roof)
+        return {
+            "bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(rounds, n),
+            "kernel": "k_crypt_blocks", "launch_ms": round(k_ms, 4),
+            "int32": {"achieved_tops": round(achieved * 1e9 * opb / 1e12, 3),
+                      "peak_tops": round(peaks["arx_mix"] / 1e12, 3),
+                      "ops_per_page": ops_per_page(rounds), "roof_gbs": round(int_roof, 1),
+                      "peak_source": "pc_intpeak(arx_mix): the reference quarter-round op stream at full "
+                                     "ILP, no memory, measured in this run"},
+            "hbm": {"achieved_gbs": round(2 * achieved, 1), "peak_gbs": hbm_peak, "peak_source": hbm_src,
+                    "algorithmic_bytes_per_page": 2 * PAGE, "roof_gbs": round(hbm_roof, 1)},
+            "measured_int_peaks_tops": {k: round(v / 1e12, 3) for k, v in peaks.items()},
+        }
+
+    rl = roofline(args.rounds, kernel_ms)
+
+    # e2e: the public host API on pinned host pages, copies inside the timed region
+    host_in = torch.empty((n, PAGE), dtype=torch.uint8).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    host_in.copy_(pages)
+    eng = pc.default_engine(local_rank)
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(3):
+        pc.crypt_pages(key, vaddr0, 1, host_in, out=host_out, rounds=args.rounds, engine=eng)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        pc.crypt_pages(key, vaddr0, 1, host_in, out=host_out, rounds=args.rounds, engine=eng)
+    e2e_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(e2e_s, device=dev)
+    e2e = {"value": round(world * bytes_per_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": bytes_per_step, "d2h_bytes_per_step": bytes_per_step,
+           "steps": e2e_steps, "path": "crypt_pages(DeviceKey, pinned torch CPU tensors) -> "
+           f"pc_crypt_pages_host, {eng.n_streams} streams x {eng.chunk_pages}-page chunks"}
+    chunks = -(-n // eng.chunk_pages)
+
+    extras = {}
+    if not args.no_extras:
+        for r in (8, 12):
+            if r == args.rounds:
+                continue
+            ms = timed(r, max(5, args.steps // 2), 3) / max(5, args.steps // 2)
+            t = max_over_ranks(ms, device=dev)
+            extras[f"chacha{r}"] = {"value": round(world * bytes_per_step / (t / 1e3) / 1e9, 2),
+                                    "unit": "GB/s", "roofline": roofline(r, ms)}
+        if rank == 0:
+            extras["latency_host_small"] = latency_sweep(pc, key, local_rank)
+    del host_in, host_out
+
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = cpu_port_rate(args.rounds, args.cpu_seconds, len(os.sched_getaffinity(0)))
+
+    key.destroy()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (uniform random pages, seed 1+rank; key from DeviceKey.generate)",
+            "config": workload_config(args, world),
+            "roofline": rl, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps + e2e_steps * chunks,
+            "gpu_launches_detail": {"device_timed": args.steps, "e2e_timed": e2e_steps * chunks},
+            "clocks": clk.summary(), "gpu": torch.cuda.get_device_name(dev),
+            "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy, read+write)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def _ncu_traffic(rounds: int, n_pages: int):
+    """dram read+write bytes per launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get(f"chacha{rounds}")
+        if e and e.get("pages") == n_pages:
+            return e["dram_bytes"]
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
+    """BASELINE configs[3]: 1-64 host-resident pages per call (the fault
+    handler's sliding window), pinned staging, p50/p99 per call."""
+    import torch
+
+    res = {}
+    for n in (1, 2, 4, 8, 16, 32, 64):
+        src = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8).pin_memory()
+        dst = torch.empty_like(src).pin_memory()
+        for _ in range(20):
+            pc.crypt_pages(key, BASE_VADDR, 1, src, out=dst)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter_ns()
+            pc.crypt_pages(key, BASE_VADDR, 1, src, out=dst)
+            ts.append(time.perf_counter_ns() - t0)
+        ts.sort()
+        p50 = ts[len(ts) // 2] / 1e3
+        res[str(n)] = {"p50_us": round(p50, 2), "p99_us": round(ts[int(len(ts) * 0.99)] / 1e3, 2),
+                       "gbps_at_p50": round(n * PAGE / (p50 * 1e-6) / 1e9, 3)}
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,133 @@
+/*
+ * pagecrypt.h -- C ABI of the B200 page-cipher engine (libpagecrypt.so).
+ *
+ * Drop-in boundary for MemShield's page-cipher hot path.  The reference
+ * (/root/reference/pkg) is a Python package with two in-process seams
+ * (SURVEY.md §8b); every entry point below names the reference interface it
+ * replaces.  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - Every function returns int: PC_OK (0) on success, else a PC_E* code;
+ *     pc_last_error() returns a thread-local message for the last failure.
+ *     The Python wrapper maps PC_EINVAL to pagecrypt's ContractViolation
+ *     (pkg/src/pagecrypt/errors.py:8-10) and everything else to
+ *     PageCryptError (errors.py:4).
+ *   - The caller owns every buffer; the library retains none after the call
+ *     (or, for *_dev entry points, after the stream reaches the call).
+ *   - rounds is 8, 12 or 20 (ChaCha8/12/20).  The reference has 20 only
+ *     (pkg/src/pagecrypt/cipher.py:158, _chacha_numba.py:68).
+ *   - Block i of page (vaddr, pid) uses the RFC 8439 state
+ *     "expand 32-byte k" || key[8] || vaddr_lo, vaddr_hi, pid, i
+ *     (pkg/src/pagecrypt/cipher.py:3-11,133-141).  Pages are 4096 bytes,
+ *     64 blocks each.  Page descriptors: per-page arrays vaddrs[n] / pids[n],
+ *     or, when an array pointer is NULL, vaddr0 + 4096*i and the scalar pid0.
+ *   - Entry points are thread-safe; a pc_engine serialises its own use.
+ */
+#ifndef PAGECRYPT_H
+#define PAGECRYPT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PC_OK 0
+#define PC_EINVAL 1 /* contract violation (bad size/alignment/rounds/handle) */
+#define PC_ECUDA 2  /* CUDA runtime/launch failure (message has the detail) */
+#define PC_ENOMEM 3 /* device or pinned allocation failed */
+#define PC_ESTATE 4 /* object used after destroy, wrong device, ... */
+
+#define PC_PAGE_SIZE 4096
+#define PC_BLOCK_SIZE 64
+#define PC_BLOCKS_PER_PAGE 64
+#define PC_KEY_SIZE 32
+
+typedef struct pc_key pc_key;       /* device-resident 256-bit master key   */
+typedef struct pc_engine pc_engine; /* per-device streams + staging buffers */
+
+/* ---- library ---------------------------------------------------------- */
+int pc_abi_version(void);          /* PC_ABI_VERSION below                 */
+const char *pc_last_error(void);   /* thread-local, never NULL             */
+int pc_device_count(int *count);
+#define PC_ABI_VERSION 1
+
+/* ---- (i) kernel seam ---------------------------------------------------
+ * Replaces pagecrypt._chacha_numba.keystream_words(kw, vaddr, pid, indices,
+ * out) (pkg/src/pagecrypt/_chacha_numba.py:44-93), consumed at
+ * pkg/src/pagecrypt/cipher.py:176-182.  Host memory in and out: kw[8] LE key
+ * words, idx[k] block indices (any int64, truncated to u32 like the
+ * reference's uint64 & 0xffffffff), out[16*k] words, block-major.
+ * Runs on the calling thread's current device; synchronous. */
+int pc_keystream_words(const uint32_t kw[8], uint64_t vaddr, uint32_t pid,
+                       const int64_t *idx, size_t k, uint32_t *out, int rounds);
+
+/* ---- (ii) raw-seed blocks ----------------------------------------------
+ * The 16-byte state tail as raw bytes (counter||nonce), one seed per block:
+ * RFC 8439 vectors that BlockSeed (cipher.py:79-104) cannot express.
+ * Mirrors pkg/tests/reference_chacha.py:28 chacha20_block_ref(key, seed16).
+ * Host memory; out = 64*k bytes. */
+int pc_keystream_raw(const uint8_t key[32], const uint8_t *seeds16, size_t k,
+                     int rounds, uint8_t *out);
+
+/* ---- (iii) key residency -----------------------------------------------
+ * Replaces WorkerPool.install_key / key slots / shutdown wipe
+ * (pkg/src/pagecrypt/workers.py:168,174-202,240-254).  The key is copied
+ * into device memory of `device`; the library keeps no host copy.
+ * pc_key_generate derives the key ON the device from 32 bytes of caller
+ * entropy mixed with device-only entropy, so the final key never exists in
+ * host RAM.  pc_key_destroy zeroes the device copy before freeing it. */
+int pc_key_install(int device, const uint8_t key[32], pc_key **out);
+int pc_key_generate(int device, const uint8_t entropy[32], pc_key **out);
+int pc_key_destroy(pc_key *key);
+int pc_key_device(const pc_key *key, int *device);
+
+/* ---- (iv) device-resident batch ----------------------------------------
+ * The batched form of cipher.crypt_page (pkg/src/pagecrypt/cipher.py:205-217)
+ * for the worker call site (pkg/src/pagecrypt/workers.py:136-138).
+ * in/out: device pointers to n*4096 bytes (16-byte aligned; in == out
+ * allowed).  vaddrs/pids: device pointers or NULL (see conventions).
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default). */
+int pc_crypt_pages_dev(const pc_key *key, const uint64_t *vaddrs, const uint32_t *pids,
+                       uint64_t vaddr0, uint32_t pid0, const void *in, void *out,
+                       size_t n, int rounds, void *stream);
+
+/* ---- (v) host-resident batch -------------------------------------------
+ * Same result over host buffers.  Pinned buffers (pc_host_alloc /
+ * pc_host_register / torch pin_memory) stream through the engine's staging
+ * ring on several CUDA streams so H2D, cipher and D2H overlap; small
+ * batches take a single-launch path.  vaddrs/pids: host arrays or NULL.
+ * Synchronous: returns when out holds the result.  `key` may be NULL when
+ * raw_key is given (caller-key mode: the engine copies raw_key into a device
+ * slot for this call and zeroes it before returning). */
+int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **out);
+int pc_engine_destroy(pc_engine *eng);
+int pc_crypt_pages_host(pc_engine *eng, const pc_key *key, const uint8_t *raw_key,
+                        const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
+                        uint32_t pid0, const void *in, void *out, size_t n, int rounds);
+
+/* ---- (vi) multi-device partition ---------------------------------------
+ * Contiguous page range [g*n/G, (g+1)*n/G) per engine g, each with its own
+ * device key (keys[g] must live on engines[g]'s device); no collective.
+ * Host buffers; one host thread per device; synchronous. */
+int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, int n_dev,
+                         const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
+                         uint32_t pid0, const void *in, void *out, size_t n, int rounds);
+
+/* ---- pinned host memory helpers --------------------------------------- */
+int pc_host_alloc(size_t bytes, void **out);
+int pc_host_free(void *p);
+int pc_host_register(void *p, size_t bytes);
+int pc_host_unregister(void *p);
+
+/* ---- measurement ------------------------------------------------------- */
+/* Integer-pipe microbenchmark used for the roofline denominator: runs `kind`
+ * (0 = LOP3 chains, 1 = IADD chains, 2 = IMAD chains, 3 = SHF rotates,
+ * 4 = ChaCha-like ARX mix) on `device` and returns measured int32 lane-ops/s. */
+int pc_intpeak(int device, int kind, double *ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAGECRYPT_H */

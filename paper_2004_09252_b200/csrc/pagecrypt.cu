@@ -1,0 +1,682 @@
+// pagecrypt.cu -- host side of libpagecrypt.so: the C ABI in include/pagecrypt.h.
+//
+// Replaces the reference's two in-process seams:
+//   kernel seam  pkg/src/pagecrypt/_chacha_numba.py:44-93  -> pc_keystream_words
+//   API seam     pkg/src/pagecrypt/cipher.py:188-249       -> pc_crypt_pages_{dev,host}
+// and the host side of the crypto worker service
+// (pkg/src/pagecrypt/workers.py: key slots :168,174-202,240-254; routing
+// :204-206 -> the page-range partitioner pc_crypt_pages_multi).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/pagecrypt.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err = "";
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(e_ == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA, "%s: %s (%s:%d)",  \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+  } while (0)
+
+// Volatile wipe the compiler cannot elide (key material in host memory).
+void wipe(void *p, size_t n) {
+  volatile uint8_t *v = static_cast<volatile uint8_t *>(p);
+  for (size_t i = 0; i < n; ++i) v[i] = 0;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) {
+      err = cudaSetDevice(dev);
+      changed = (err == cudaSuccess);
+    }
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+bool valid_rounds(int r) { return r == 8 || r == 12 || r == 20; }
+
+int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+// Tuning knobs (fixed at first use; env overrides are for measurement).
+struct Tuning {
+  int add_mode;    // pc::AddMode for the crypt kernel
+  int small_mode;  // 0 = staged copies, 1 = zero-copy on mapped pinned memory
+  size_t small_max;
+};
+const Tuning &tuning() {
+  static const Tuning t = {env_int("PAGECRYPT_ADDMODE", pc::kAddAlu),
+                           env_int("PAGECRYPT_SMALL_MODE", 1),
+                           static_cast<size_t>(env_int("PAGECRYPT_SMALL_MAX", 64))};
+  return t;
+}
+
+template <int R>
+void launch_crypt_r(int am, const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
+                    uint64_t n_blocks, cudaStream_t st) {
+  const dim3 block(256);
+  const dim3 grid(static_cast<unsigned>((n_blocks + 255) / 256));
+  auto i4 = static_cast<const uint4 *>(in);
+  auto o4 = static_cast<uint4 *>(out);
+  switch (am) {
+    case pc::kAddFma: pc::k_crypt_blocks<R, pc::kAddFma><<<grid, block, 0, st>>>(key, d, i4, o4, n_blocks, 1u); break;
+    case pc::kAddSplitA: pc::k_crypt_blocks<R, pc::kAddSplitA><<<grid, block, 0, st>>>(key, d, i4, o4, n_blocks, 1u); break;
+    default: pc::k_crypt_blocks<R, pc::kAddAlu><<<grid, block, 0, st>>>(key, d, i4, o4, n_blocks, 1u); break;
+  }
+}
+
+int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
+                 size_t n_pages, int rounds, cudaStream_t st) {
+  if (n_pages == 0) return PC_OK;
+  const uint64_t n_blocks = static_cast<uint64_t>(n_pages) * PC_BLOCKS_PER_PAGE;
+  const int am = tuning().add_mode;
+  switch (rounds) {
+    case 8: launch_crypt_r<8>(am, key, d, in, out, n_blocks, st); break;
+    case 12: launch_crypt_r<12>(am, key, d, in, out, n_blocks, st); break;
+    default: launch_crypt_r<20>(am, key, d, in, out, n_blocks, st); break;
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+int launch_keystream(const uint32_t *key, const uint32_t *seeds, size_t k, uint32_t *out, int rounds,
+                     cudaStream_t st) {
+  const dim3 block(128);
+  const dim3 grid(static_cast<unsigned>((k + 127) / 128));
+  switch (rounds) {
+    case 8: pc::k_keystream_seeds<8><<<grid, block, 0, st>>>(key, seeds, k, out); break;
+    case 12: pc::k_keystream_seeds<12><<<grid, block, 0, st>>>(key, seeds, k, out); break;
+    default: pc::k_keystream_seeds<20><<<grid, block, 0, st>>>(key, seeds, k, out); break;
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+// Is p host memory the device can address (pinned / registered)?  Returns the
+// device-visible alias in *dev (nullptr when not pinned).
+bool pinned_alias(const void *p, void **dev) {
+  *dev = nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return false;
+  *dev = a.devicePointer;
+  return true;
+}
+
+// Scratch for the synchronous keystream seams, one per device (guarded).
+struct Scratch {
+  std::mutex mu;
+  void *d = nullptr;
+  size_t cap = 0;
+  cudaStream_t st = nullptr;
+};
+Scratch &scratch(int dev) {
+  static Scratch s[64];
+  return s[dev & 63];
+}
+
+int keystream_sync(const uint32_t kw[8], const uint32_t *seeds, size_t k, uint32_t *out, int rounds) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  Scratch &sc = scratch(dev);
+  std::lock_guard<std::mutex> lk(sc.mu);
+  const size_t in_bytes = 32 + 16 * k;
+  const size_t need = 256 + 16 * k + 64 * k;
+  if (!sc.st) CU(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+  if (sc.cap < need) {
+    if (sc.d) CU(cudaFree(sc.d));
+    sc.d = nullptr;
+    sc.cap = 0;
+    CU(cudaMalloc(&sc.d, need));
+    sc.cap = need;
+  }
+  std::vector<uint32_t> host(in_bytes / 4);
+  std::memcpy(host.data(), kw, 32);
+  std::memcpy(host.data() + 8, seeds, 16 * k);
+  uint8_t *d = static_cast<uint8_t *>(sc.d);
+  // key at d[0..32), seeds at d+256, out after the seeds
+  int rc = PC_OK;
+  cudaError_t e = cudaMemcpyAsync(d, host.data(), 32, cudaMemcpyHostToDevice, sc.st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d + 256, host.data() + 8, 16 * k, cudaMemcpyHostToDevice, sc.st);
+  if (e == cudaSuccess) {
+    rc = launch_keystream(reinterpret_cast<uint32_t *>(d), reinterpret_cast<uint32_t *>(d + 256), k,
+                          reinterpret_cast<uint32_t *>(d + 256 + 16 * k), rounds, sc.st);
+    if (rc == PC_OK)
+      e = cudaMemcpyAsync(out, d + 256 + 16 * k, 64 * k, cudaMemcpyDeviceToHost, sc.st);
+  }
+  cudaError_t e2 = cudaMemsetAsync(d, 0, need, sc.st); // wipe key + keystream
+  cudaError_t e3 = cudaStreamSynchronize(sc.st);
+  wipe(host.data(), 32);
+  if (rc != PC_OK) return rc;
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = e3;
+  CU(e);
+  return PC_OK;
+}
+
+constexpr uint32_t kKeyMagic = 0x6b657931u;    // "key1"
+constexpr uint32_t kEngineMagic = 0x656e6731u; // "eng1"
+
+} // namespace
+
+struct pc_key {
+  uint32_t magic;
+  int device;
+  uint32_t *d_words;
+};
+
+struct pc_engine {
+  uint32_t magic = kEngineMagic;
+  int device = 0;
+  int n_streams = 0;
+  size_t chunk_pages = 0;
+  std::mutex mu;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> done;
+  std::vector<uint8_t *> d_pages;   // per-stream device staging, chunk_pages*4096
+  std::vector<uint64_t *> d_vaddrs; // per-stream descriptor staging
+  std::vector<uint32_t *> d_pids;
+  std::vector<uint8_t *> h_bounce;  // pinned bounce for pageable I/O (lazy)
+  std::vector<uint8_t *> h_desc;    // pinned descriptor staging (chunk*12 bytes)
+  uint8_t *h_key = nullptr;         // pinned 256-B raw-key staging
+  uint32_t *d_rawkey = nullptr;     // caller-key device slot (wiped after use)
+  // small-batch path: one pinned+mapped region and its device mirror
+  uint8_t *h_small = nullptr;
+  uint8_t *hd_small = nullptr;      // device alias of h_small (zero-copy)
+  uint8_t *d_small = nullptr;
+  size_t small_bytes = 0;
+};
+
+// ===========================================================================
+extern "C" {
+
+int pc_abi_version(void) { return PC_ABI_VERSION; }
+
+const char *pc_last_error(void) { return g_err.c_str(); }
+
+int pc_device_count(int *count) {
+  if (!count) return fail(PC_EINVAL, "count is NULL");
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(PC_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  return PC_OK;
+}
+
+// ---- (i) kernel seam -------------------------------------------------------
+int pc_keystream_words(const uint32_t kw[8], uint64_t vaddr, uint32_t pid, const int64_t *idx,
+                       size_t k, uint32_t *out, int rounds) {
+  if (!kw) return fail(PC_EINVAL, "key words are NULL");
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  if (k == 0) return PC_OK;
+  if (!idx || !out) return fail(PC_EINVAL, "indices/out are NULL");
+  std::vector<uint32_t> seeds(4 * k);
+  for (size_t i = 0; i < k; ++i) {
+    seeds[4 * i + 0] = static_cast<uint32_t>(vaddr);
+    seeds[4 * i + 1] = static_cast<uint32_t>(vaddr >> 32);
+    seeds[4 * i + 2] = pid;
+    seeds[4 * i + 3] = static_cast<uint32_t>(static_cast<uint64_t>(idx[i]));
+  }
+  return keystream_sync(kw, seeds.data(), k, out, rounds);
+}
+
+// ---- (ii) raw seeds --------------------------------------------------------
+int pc_keystream_raw(const uint8_t key[32], const uint8_t *seeds16, size_t k, int rounds, uint8_t *out) {
+  if (!key) return fail(PC_EINVAL, "key is NULL");
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  if (k == 0) return PC_OK;
+  if (!seeds16 || !out) return fail(PC_EINVAL, "seeds/out are NULL");
+  uint32_t kw[8];
+  std::memcpy(kw, key, 32);
+  std::vector<uint32_t> seeds(4 * k);
+  std::memcpy(seeds.data(), seeds16, 16 * k);
+  std::vector<uint32_t> words(16 * k);
+  int rc = keystream_sync(kw, seeds.data(), k, words.data(), rounds);
+  wipe(kw, sizeof kw);
+  if (rc == PC_OK) std::memcpy(out, words.data(), 64 * k);
+  wipe(words.data(), 64 * k);
+  return rc;
+}
+
+// ---- (iii) key residency ---------------------------------------------------
+int pc_key_install(int device, const uint8_t key[32], pc_key **out) {
+  if (!key || !out) return fail(PC_EINVAL, "key/out is NULL");
+  *out = nullptr;
+  DeviceGuard g(device);
+  CU(g.err);
+  uint32_t *d = nullptr;
+  CU(cudaMalloc(&d, 256));
+  cudaError_t e = cudaMemcpy(d, key, 32, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    CU(e);
+  }
+  *out = new pc_key{kKeyMagic, device, d};
+  return PC_OK;
+}
+
+int pc_key_generate(int device, const uint8_t entropy[32], pc_key **out) {
+  if (!entropy || !out) return fail(PC_EINVAL, "entropy/out is NULL");
+  *out = nullptr;
+  DeviceGuard g(device);
+  CU(g.err);
+  uint32_t *d = nullptr;
+  CU(cudaMalloc(&d, 256));
+  // entropy at d[32..63] (scratch), key at d[0..31]
+  cudaError_t e = cudaMemcpy(d + 8, entropy, 32, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    pc::k_keygen<<<1, 1>>>(d + 8, d);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemset(d + 8, 0, 32);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaMemset(d, 0, 256);
+    cudaFree(d);
+    CU(e);
+  }
+  *out = new pc_key{kKeyMagic, device, d};
+  return PC_OK;
+}
+
+int pc_key_destroy(pc_key *key) {
+  if (!key) return PC_OK;
+  if (key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  DeviceGuard g(key->device);
+  CU(g.err);
+  // wait for every stream that may still read the key, then zero and free it
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemset(key->d_words, 0, 256));
+  CU(cudaDeviceSynchronize());
+  CU(cudaFree(key->d_words));
+  key->magic = 0;
+  key->d_words = nullptr;
+  delete key;
+  return PC_OK;
+}
+
+int pc_key_device(const pc_key *key, int *device) {
+  if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  if (!device) return fail(PC_EINVAL, "device is NULL");
+  *device = key->device;
+  return PC_OK;
+}
+
+// ---- (iv) device-resident batch -------------------------------------------
+int pc_crypt_pages_dev(const pc_key *key, const uint64_t *vaddrs, const uint32_t *pids,
+                       uint64_t vaddr0, uint32_t pid0, const void *in, void *out, size_t n,
+                       int rounds, void *stream) {
+  if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  if (n == 0) return PC_OK;
+  if (!in || !out) return fail(PC_EINVAL, "in/out is NULL");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(PC_EINVAL, "page buffers must be 16-byte aligned");
+  if (!vaddrs && (vaddr0 & 4095)) return fail(PC_EINVAL, "vaddr0 %#llx not page-aligned", (unsigned long long)vaddr0);
+  if (!vaddrs && n > 1 && vaddr0 + 4096ull * (n - 1) < vaddr0)
+    return fail(PC_EINVAL, "contiguous vaddr range overflows u64");
+  DeviceGuard g(key->device);
+  CU(g.err);
+  const pc::PageDesc d{vaddrs, pids, vaddr0, pid0};
+  return launch_crypt(key->d_words, d, in, out, n, rounds, static_cast<cudaStream_t>(stream));
+}
+
+// ---- (v) host-resident batch ---------------------------------------------
+int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **out) {
+  if (!out) return fail(PC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_streams <= 0) n_streams = 4;
+  if (n_streams > 16) n_streams = 16;
+  if (chunk_pages == 0) chunk_pages = 2048; // 8 MiB per stage
+  DeviceGuard g(device);
+  CU(g.err);
+  auto *e = new pc_engine();
+  e->device = device;
+  e->n_streams = n_streams;
+  e->chunk_pages = chunk_pages;
+  auto cleanup = [&](int rc) {
+    pc_engine_destroy(e);
+    return rc;
+  };
+#define CUE(call)                                                                           \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return cleanup(fail(e_ == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA, "%s: %s", \
+                          #call, cudaGetErrorString(e_)));                                  \
+  } while (0)
+  e->streams.assign(n_streams, nullptr);
+  e->done.assign(n_streams, nullptr);
+  e->d_pages.assign(n_streams, nullptr);
+  e->d_vaddrs.assign(n_streams, nullptr);
+  e->d_pids.assign(n_streams, nullptr);
+  e->h_bounce.assign(n_streams, nullptr);
+  e->h_desc.assign(n_streams, nullptr);
+  for (int s = 0; s < n_streams; ++s) {
+    CUE(cudaStreamCreateWithFlags(&e->streams[s], cudaStreamNonBlocking));
+    CUE(cudaEventCreateWithFlags(&e->done[s], cudaEventDisableTiming));
+    CUE(cudaMalloc(&e->d_pages[s], chunk_pages * PC_PAGE_SIZE));
+    CUE(cudaMalloc(&e->d_vaddrs[s], chunk_pages * 8));
+    CUE(cudaMalloc(&e->d_pids[s], chunk_pages * 4));
+    CUE(cudaHostAlloc(&e->h_desc[s], chunk_pages * 12, cudaHostAllocDefault));
+  }
+  CUE(cudaHostAlloc(&e->h_key, 256, cudaHostAllocDefault));
+  CUE(cudaMalloc(&e->d_rawkey, 256));
+  const size_t sm = tuning().small_max;
+  e->small_bytes = 256 + sm * 16 + sm * PC_PAGE_SIZE;
+  CUE(cudaHostAlloc(&e->h_small, e->small_bytes, cudaHostAllocMapped));
+  CUE(cudaHostGetDevicePointer(reinterpret_cast<void **>(&e->hd_small), e->h_small, 0));
+  CUE(cudaMalloc(&e->d_small, e->small_bytes));
+#undef CUE
+  *out = e;
+  return PC_OK;
+}
+
+int pc_engine_destroy(pc_engine *e) {
+  if (!e) return PC_OK;
+  if (e->magic != kEngineMagic) return fail(PC_ESTATE, "not a live pc_engine");
+  DeviceGuard g(e->device);
+  for (auto s : e->streams)
+    if (s) cudaStreamSynchronize(s);
+  if (e->d_rawkey) { cudaMemset(e->d_rawkey, 0, 256); cudaDeviceSynchronize(); cudaFree(e->d_rawkey); }
+  if (e->h_key) { wipe(e->h_key, 256); cudaFreeHost(e->h_key); }
+  if (e->h_small) { wipe(e->h_small, 256); cudaFreeHost(e->h_small); }
+  if (e->d_small) cudaFree(e->d_small);
+  for (size_t s = 0; s < e->streams.size(); ++s) {
+    if (e->d_pages[s]) cudaFree(e->d_pages[s]);
+    if (e->d_vaddrs[s]) cudaFree(e->d_vaddrs[s]);
+    if (e->d_pids[s]) cudaFree(e->d_pids[s]);
+    if (e->h_bounce[s]) cudaFreeHost(e->h_bounce[s]);
+    if (e->h_desc[s]) cudaFreeHost(e->h_desc[s]);
+    if (e->done[s]) cudaEventDestroy(e->done[s]);
+    if (e->streams[s]) cudaStreamDestroy(e->streams[s]);
+  }
+  cudaGetLastError();
+  e->magic = 0;
+  delete e;
+  return PC_OK;
+}
+
+namespace {
+
+// Small batches: one staging region [key | vaddrs | pids | pages] in pinned,
+// mapped memory.  Zero-copy mode runs the kernel directly on it (one launch,
+// no copies); copy mode does one H2D, the kernel and one D2H.
+int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, const uint64_t *vaddrs,
+                const uint32_t *pids, uint64_t vaddr0, uint32_t pid0, const void *in, void *out,
+                size_t n, int rounds) {
+  const size_t off_v = 256, off_p = off_v + ((n * 8 + 255) & ~size_t(255));
+  const size_t off_pg = off_p + ((n * 4 + 255) & ~size_t(255));
+  const size_t used = off_pg + n * PC_PAGE_SIZE;
+  uint8_t *h = e->h_small;
+  if (raw_key) std::memcpy(h, raw_key, 32);
+  if (vaddrs) std::memcpy(h + off_v, vaddrs, n * 8);
+  if (pids) std::memcpy(h + off_p, pids, n * 4);
+  std::memcpy(h + off_pg, in, n * PC_PAGE_SIZE);
+  cudaStream_t st = e->streams[0];
+  const bool zc = tuning().small_mode == 1;
+  uint8_t *base = zc ? e->hd_small : e->d_small;
+  const pc::PageDesc d{vaddrs ? reinterpret_cast<const uint64_t *>(base + off_v) : nullptr,
+                       pids ? reinterpret_cast<const uint32_t *>(base + off_p) : nullptr, vaddr0, pid0};
+  const uint32_t *key = raw_key ? reinterpret_cast<const uint32_t *>(base) : dkey;
+  int rc = PC_OK;
+  cudaError_t err = cudaSuccess;
+  if (!zc) err = cudaMemcpyAsync(e->d_small, h, used, cudaMemcpyHostToDevice, st);
+  if (err == cudaSuccess) rc = launch_crypt(key, d, base + off_pg, base + off_pg, n, rounds, st);
+  if (err == cudaSuccess && rc == PC_OK && !zc)
+    err = cudaMemcpyAsync(h + off_pg, e->d_small + off_pg, n * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, st);
+  if (!zc && raw_key) {
+    cudaError_t e2 = cudaMemsetAsync(e->d_small, 0, 256, st);
+    if (err == cudaSuccess) err = e2;
+  }
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  if (raw_key) wipe(h, 32);
+  if (rc != PC_OK) return rc;
+  if (err == cudaSuccess) err = e3;
+  CU(err);
+  std::memcpy(out, h + off_pg, n * PC_PAGE_SIZE);
+  return PC_OK;
+}
+
+int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const uint32_t *pids,
+                uint64_t vaddr0, uint32_t pid0, const void *in, void *out, size_t n, int rounds) {
+  void *in_dev = nullptr, *out_dev = nullptr;
+  const bool pin_in = pinned_alias(in, &in_dev);
+  const bool pin_out = pinned_alias(out, &out_dev);
+  const bool has_desc = vaddrs || pids;
+  const int S = e->n_streams;
+  const size_t C = e->chunk_pages;
+  if (!pin_in || !pin_out) {
+    for (int s = 0; s < S; ++s)
+      if (!e->h_bounce[s]) CU(cudaHostAlloc(&e->h_bounce[s], C * PC_PAGE_SIZE, cudaHostAllocDefault));
+  }
+  const size_t n_chunks = (n + C - 1) / C;
+  auto *src_b = static_cast<const uint8_t *>(in);
+  auto *dst_b = static_cast<uint8_t *>(out);
+  auto finish = [&](size_t c) -> int { // chunk c's stream slot is about to be reused / drained
+    const int s = static_cast<int>(c % S);
+    CU(cudaEventSynchronize(e->done[s]));
+    if (!pin_out) {
+      const size_t p0 = c * C, m = std::min(C, n - p0);
+      std::memcpy(dst_b + p0 * PC_PAGE_SIZE, e->h_bounce[s], m * PC_PAGE_SIZE);
+    }
+    return PC_OK;
+  };
+  for (size_t c = 0; c < n_chunks; ++c) {
+    const int s = static_cast<int>(c % S);
+    cudaStream_t st = e->streams[s];
+    const size_t p0 = c * C, m = std::min(C, n - p0);
+    if (c >= static_cast<size_t>(S) && (!pin_in || !pin_out || has_desc)) {
+      int rc = finish(c - S);
+      if (rc != PC_OK) return rc;
+    }
+    const uint8_t *src = src_b + p0 * PC_PAGE_SIZE;
+    if (!pin_in) {
+      std::memcpy(e->h_bounce[s], src, m * PC_PAGE_SIZE);
+      src = e->h_bounce[s];
+    }
+    CU(cudaMemcpyAsync(e->d_pages[s], src, m * PC_PAGE_SIZE, cudaMemcpyHostToDevice, st));
+    pc::PageDesc d{nullptr, nullptr, vaddr0 + 4096ull * p0, pid0};
+    if (vaddrs) {
+      std::memcpy(e->h_desc[s], vaddrs + p0, m * 8);
+      CU(cudaMemcpyAsync(e->d_vaddrs[s], e->h_desc[s], m * 8, cudaMemcpyHostToDevice, st));
+      d.vaddrs = e->d_vaddrs[s];
+    }
+    if (pids) {
+      std::memcpy(e->h_desc[s] + C * 8, pids + p0, m * 4);
+      CU(cudaMemcpyAsync(e->d_pids[s], e->h_desc[s] + C * 8, m * 4, cudaMemcpyHostToDevice, st));
+      d.pids = e->d_pids[s];
+    }
+    int rc = launch_crypt(key, d, e->d_pages[s], e->d_pages[s], m, rounds, st);
+    if (rc != PC_OK) return rc;
+    uint8_t *dst = pin_out ? dst_b + p0 * PC_PAGE_SIZE : e->h_bounce[s];
+    CU(cudaMemcpyAsync(dst, e->d_pages[s], m * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(e->done[s], st));
+  }
+  const size_t first_pending =
+      (!pin_in || !pin_out || has_desc) && n_chunks > static_cast<size_t>(S) ? n_chunks - S : 0;
+  for (size_t c = first_pending; c < n_chunks; ++c) {
+    int rc = finish(c);
+    if (rc != PC_OK) return rc;
+  }
+  return PC_OK;
+}
+
+} // namespace
+
+int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key, const uint64_t *vaddrs,
+                        const uint32_t *pids, uint64_t vaddr0, uint32_t pid0, const void *in, void *out,
+                        size_t n, int rounds) {
+  if (!e || e->magic != kEngineMagic) return fail(PC_ESTATE, "not a live pc_engine");
+  if (!raw_key && (!key || key->magic != kKeyMagic)) return fail(PC_ESTATE, "not a live pc_key");
+  if (!raw_key && key->device != e->device)
+    return fail(PC_EINVAL, "key lives on device %d, engine on device %d", key->device, e->device);
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  if (n == 0) return PC_OK;
+  if (!in || !out) return fail(PC_EINVAL, "in/out is NULL");
+  if (!vaddrs && (vaddr0 & 4095)) return fail(PC_EINVAL, "vaddr0 %#llx not page-aligned", (unsigned long long)vaddr0);
+  if (vaddrs)
+    for (size_t i = 0; i < n; ++i)
+      if (vaddrs[i] & 4095) return fail(PC_EINVAL, "vaddr %#llx not page-aligned", (unsigned long long)vaddrs[i]);
+  std::lock_guard<std::mutex> lk(e->mu);
+  DeviceGuard g(e->device);
+  CU(g.err);
+  if (n <= tuning().small_max)
+    return crypt_small(e, raw_key ? nullptr : key->d_words, raw_key, vaddrs, pids, vaddr0, pid0, in, out, n, rounds);
+  const uint32_t *dkey = nullptr;
+  if (raw_key) {
+    std::memcpy(e->h_key, raw_key, 32);
+    cudaError_t err = cudaMemcpyAsync(e->d_rawkey, e->h_key, 32, cudaMemcpyHostToDevice, e->streams[0]);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(e->streams[0]);
+    wipe(e->h_key, 32);
+    CU(err);
+    dkey = e->d_rawkey;
+  } else {
+    dkey = key->d_words;
+  }
+  int rc = crypt_large(e, dkey, vaddrs, pids, vaddr0, pid0, in, out, n, rounds);
+  if (raw_key) {
+    // drain every stream that may read the slot, then zero it
+    for (auto s : e->streams) cudaStreamSynchronize(s);
+    cudaError_t err = cudaMemsetAsync(e->d_rawkey, 0, 256, e->streams[0]);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(e->streams[0]);
+    if (rc == PC_OK) CU(err);
+  }
+  return rc;
+}
+
+// ---- (vi) multi-device partition --------------------------------------------
+int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, int n_dev,
+                         const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0, uint32_t pid0,
+                         const void *in, void *out, size_t n, int rounds) {
+  if (!engines || !keys || n_dev <= 0) return fail(PC_EINVAL, "need >= 1 engine and key");
+  std::vector<int> rcs(n_dev, PC_OK);
+  std::vector<std::string> errs(n_dev);
+  std::vector<std::thread> th;
+  for (int g = 0; g < n_dev; ++g) {
+    th.emplace_back([&, g] {
+      const size_t lo = n * g / n_dev, hi = n * (g + 1) / n_dev;
+      if (hi == lo) return;
+      rcs[g] = pc_crypt_pages_host(engines[g], keys[g], nullptr, vaddrs ? vaddrs + lo : nullptr,
+                                   pids ? pids + lo : nullptr, vaddr0 + 4096ull * lo, pid0,
+                                   static_cast<const uint8_t *>(in) + lo * PC_PAGE_SIZE,
+                                   static_cast<uint8_t *>(out) + lo * PC_PAGE_SIZE, hi - lo, rounds);
+      if (rcs[g] != PC_OK) errs[g] = pc_last_error();
+    });
+  }
+  for (auto &t : th) t.join();
+  for (int g = 0; g < n_dev; ++g)
+    if (rcs[g] != PC_OK) return fail(rcs[g], "device slot %d: %s", g, errs[g].c_str());
+  return PC_OK;
+}
+
+// ---- pinned memory ---------------------------------------------------------
+int pc_host_alloc(size_t bytes, void **out) {
+  if (!out) return fail(PC_EINVAL, "out is NULL");
+  *out = nullptr;
+  CU(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
+  return PC_OK;
+}
+int pc_host_free(void *p) {
+  if (p) CU(cudaFreeHost(p));
+  return PC_OK;
+}
+int pc_host_register(void *p, size_t bytes) {
+  if (!p || !bytes) return fail(PC_EINVAL, "null/empty range");
+  CU(cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+  return PC_OK;
+}
+int pc_host_unregister(void *p) {
+  if (!p) return fail(PC_EINVAL, "null pointer");
+  CU(cudaHostUnregister(p));
+  return PC_OK;
+}
+
+// ---- measurement -------------------------------------------------------------
+int pc_intpeak(int device, int kind, double *ops_per_s) {
+  if (!ops_per_s) return fail(PC_EINVAL, "ops_per_s is NULL");
+  if (kind < 0 || kind > 5) return fail(PC_EINVAL, "kind must be 0..5");
+  DeviceGuard g(device);
+  CU(g.err);
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  uint32_t *sink = nullptr;
+  CU(cudaMalloc(&sink, 1024 * 4));
+  const dim3 grid(sms * 8), block(256);
+  const int iters = kind >= 4 ? 1000 : 1500;
+  auto run = [&](int it) {
+    switch (kind) {
+      case 0: pc::k_intpeak<0><<<grid, block>>>(1u, 1u, it, sink); break;
+      case 1: pc::k_intpeak<1><<<grid, block>>>(1u, 1u, it, sink); break;
+      case 2: pc::k_intpeak<2><<<grid, block>>>(1u, 1u, it, sink); break;
+      case 3: pc::k_intpeak<3><<<grid, block>>>(1u, 1u, it, sink); break;
+      case 4: pc::k_intpeak<4><<<grid, block>>>(1u, 1u, it, sink); break;
+      default: pc::k_intpeak<5><<<grid, block>>>(1u, 1u, it, sink); break;
+    }
+  };
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  run(iters / 10); // warm-up
+  float best_ms = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    CU(cudaEventRecord(a));
+    run(iters);
+    CU(cudaEventRecord(b));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    best_ms = std::min(best_ms, ms);
+  }
+  CU(cudaGetLastError());
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  const double ops_per_iter = kind >= 4 ? 16.0 * 12.0 : 16.0 * 8.0;
+  *ops_per_s = static_cast<double>(grid.x) * block.x * iters * ops_per_iter / (best_ms * 1e-3);
+  return PC_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,82 @@
+"""Multi-GPU page-range partitioner (no collective on the data path).
+
+Each block's keystream depends only on (key, vaddr, pid, block index)
+(pkg/src/pagecrypt/cipher.py:133-141), so any partition of a batch is
+bit-identical to processing it in one piece -- the same property the
+reference shows for 1 vs 8 workers (pkg/tests/test_workers.py:136-148).  The
+reference routes whole clients to workers (``WorkerPool.route``,
+pkg/src/pagecrypt/workers.py:204-206); for page batches the B200 analog is a
+contiguous page range per GPU, each GPU holding its own copy of the key (the
+per-worker key slots, workers.py:167-169,193-195).
+
+Two launch shapes:
+
+* one process per GPU (torchrun): :func:`shard` gives rank r its range; the
+  only cross-rank traffic is the benchmark's barrier and max-over-ranks time
+  (:func:`max_over_ranks`), never page data;
+* one process, several GPUs: :func:`crypt_pages_multi` drives
+  ``pc_crypt_pages_multi`` (one host thread per device, host-resident pages).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .engine import DeviceKey, Engine, _host_pids, _host_vaddrs, PAGE_SIZE
+from .errors import ContractViolation
+
+
+def page_ranges(n: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous [lo, hi) ranges, sizes differing by at most one page."""
+    if parts < 1:
+        raise ContractViolation(f"parts must be >= 1, got {parts}")
+    if n < 0:
+        raise ContractViolation("negative page count")
+    return [(n * g // parts, n * (g + 1) // parts) for g in range(parts)]
+
+
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    if not 0 <= rank < world:
+        raise ContractViolation(f"rank {rank} outside world of {world}")
+    return page_ranges(n, world)[rank]
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank scalar over the default process group (the bench's
+    timing reduction); identity when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def crypt_pages_multi(keys: list[DeviceKey], engines: list[Engine], vaddrs, pids,
+                      pages: np.ndarray, out: np.ndarray | None = None, *, rounds: int = 20) -> np.ndarray:
+    """Host-resident batch split by contiguous page range over len(engines)
+    devices (keys[g] must live on engines[g]'s device)."""
+    if len(keys) != len(engines) or not engines:
+        raise ContractViolation("need one key per engine")
+    for k, e in zip(keys, engines):
+        if k.device != e.device:
+            raise ContractViolation(f"key on device {k.device}, engine on {e.device}")
+    arr = np.ascontiguousarray(pages, dtype=np.uint8).reshape(-1, PAGE_SIZE)
+    n = arr.shape[0]
+    if out is None:
+        out = np.empty_like(arr)
+    v_arr, vaddr0 = _host_vaddrs(vaddrs, n)
+    p_arr, pid0 = _host_pids(pids, n)
+    G = len(engines)
+    eh = (ctypes.c_void_p * G)(*[e.handle for e in engines])
+    kh = (ctypes.c_void_p * G)(*[k.handle for k in keys])
+    _native.call("pc_crypt_pages_multi", eh, kh, G,
+                 None if v_arr is None else v_arr.ctypes.data,
+                 None if p_arr is None else p_arr.ctypes.data,
+                 vaddr0, pid0, arr.ctypes.data, out.ctypes.data, n, rounds)
+    return out

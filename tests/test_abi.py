@@ -1,0 +1,74 @@
+"""CPU checks of the C ABI: the library loads, exports exactly what
+include/pagecrypt.h declares, and refuses to compute without a GPU (no CPU
+fallback)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2004_09252_b200 import _native
+from paper_2004_09252_b200.errors import ContractViolation, PageCryptError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pagecrypt.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(pc_\w+)\s*\(", text, flags=re.M))
+
+
+def test_header_matches_binding_table():
+    assert header_functions() == set(_native.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (pc_\w+)", out))
+    assert header_functions() <= exported
+
+
+def test_abi_version():
+    assert _native.load().pc_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _native.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_invalid_arguments_rejected_before_device_use():
+    lib = _native.load()
+    # rounds validated first: EINVAL even without a GPU
+    out = (ctypes.c_uint32 * 16)()
+    kw = (ctypes.c_uint32 * 8)()
+    idx = (ctypes.c_int64 * 1)(0)
+    rc = lib.pc_keystream_words(kw, 0, 0, idx, 1, out, 7)
+    assert rc == _native.PC_EINVAL
+    assert b"rounds" in lib.pc_last_error()
+    with pytest.raises(ContractViolation):
+        _native.check(rc)
+    # NULL handles are state errors
+    assert lib.pc_crypt_pages_dev(None, None, None, 0, 0, None, None, 1, 20, None) == _native.PC_ESTATE
+    assert lib.pc_key_destroy(None) == _native.PC_OK
+
+
+@pytest.mark.skipif(_native.device_count() > 0, reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback_without_gpu():
+    import paper_2004_09252_b200 as pc
+
+    with pytest.raises(PageCryptError):
+        pc.crypt_page(bytes(32), 0, 0, bytes(4096))
+    with pytest.raises(PageCryptError):
+        pc.page_keystream(bytes(32), 0, 0)
+    with pytest.raises(PageCryptError):
+        pc.DeviceKey.install(bytes(32), 0)

@@ -1,0 +1,248 @@
+"""GPU parity of the batched engine: device-resident and host-resident
+paths, descriptor forms, rounds, in-place, edge sizes, the key lifecycle and
+the multi-device partition -- byte-exact against the C oracle at sizes it
+finishes in seconds, and at BASELINE's 1 GiB size through size-independent
+properties (involution, keystream linearity, chunk/partition independence)."""
+
+import numpy as np
+import pytest
+
+import paper_2004_09252_b200 as pc
+from paper_2004_09252_b200 import partition
+from paper_2004_09252_b200.errors import ContractViolation, PageCryptError
+
+from oracle import coracle as C
+
+pytestmark = pytest.mark.gpu
+
+KEY = bytes.fromhex("8b034a0ee06db6c134b1c8fc867c39bae599f01835025a7acf4b57268dc7853c")
+BASE = 0x1_0000_0000
+
+
+def rand_pages(n, seed=1):
+    return np.random.default_rng(seed).integers(0, 256, size=(n, 4096), dtype=np.uint8)
+
+
+@pytest.fixture(scope="module")
+def dkey(cuda):
+    k = pc.DeviceKey.install(KEY, 0)
+    yield k
+    k.destroy()
+
+
+def t(x, device="cuda"):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device)
+
+
+class TestDevicePath:
+    @pytest.mark.parametrize("rounds", [8, 12, 20])
+    @pytest.mark.parametrize("n", [1, 3, 64, 4097])
+    def test_contiguous_scalar_pid(self, dkey, n, rounds):
+        import torch
+
+        pages = rand_pages(n, seed=n)
+        got = pc.crypt_pages(dkey, BASE, 1, t(pages), rounds=rounds)
+        torch.cuda.synchronize()
+        want = C.crypt_pages(KEY, None, None, pages, rounds=rounds, vaddr0=BASE, pid0=1, nthreads=8)
+        assert np.array_equal(got.cpu().numpy(), want)
+
+    def test_per_page_descriptors(self, dkey, ref_pages):
+        import torch
+
+        r = ref_pages
+        with pc.DeviceKey.install(r["key"].tobytes(), 0) as k:
+            got = pc.crypt_pages(k, t(r["vaddrs"].view(np.int64)), t(r["pids"].view(np.int32)), t(r["pages"]))
+            torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), r["ct"])
+
+    def test_numpy_descriptors_and_uint64(self, ref_pages):
+        import torch
+
+        r = ref_pages
+        got = pc.crypt_pages(r["key"].tobytes(), r["vaddrs"], r["pids"], t(r["pages"]))
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), r["ct"])
+
+    def test_pid_per_page_variant(self, dkey):
+        """pid = 1 + (i % 64)."""
+        import torch
+
+        n = 2048
+        pages = rand_pages(n, 3)
+        pids = (1 + np.arange(n) % 64).astype(np.uint32)
+        got = pc.crypt_pages(dkey, BASE, t(pids.view(np.int32)), t(pages))
+        torch.cuda.synchronize()
+        want = C.crypt_pages(KEY, None, pids, pages, vaddr0=BASE, nthreads=8)
+        assert np.array_equal(got.cpu().numpy(), want)
+
+    def test_in_place(self, dkey):
+        import torch
+
+        pages = rand_pages(513, 4)
+        d = t(pages)
+        out = pc.crypt_pages(dkey, BASE, 7, d, out=d)
+        torch.cuda.synchronize()
+        assert out.data_ptr() == d.data_ptr()
+        assert np.array_equal(d.cpu().numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=7, nthreads=8))
+
+    def test_empty_batch(self, dkey):
+        import torch
+
+        d = torch.empty((0, 4096), dtype=torch.uint8, device="cuda")
+        assert pc.crypt_pages(dkey, BASE, 1, d).numel() == 0
+
+    def test_side_stream(self, dkey):
+        import torch
+
+        pages = rand_pages(300, 5)
+        s = torch.cuda.Stream()
+        d = t(pages)
+        torch.cuda.current_stream().synchronize()
+        with torch.cuda.stream(s):
+            got = pc.crypt_pages(dkey, BASE, 2, d)
+        s.synchronize()
+        assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=2))
+
+    def test_unaligned_device_vaddrs_rejected(self, dkey):
+        v = t(np.array([4096, 4097], dtype=np.int64))
+        with pytest.raises(ContractViolation):
+            pc.crypt_pages(dkey, v, 1, t(rand_pages(2)))
+
+    def test_max_vaddr_and_pid(self, dkey):
+        import torch
+
+        pages = rand_pages(4, 6)
+        v0 = 2**64 - 4 * 4096
+        got = pc.crypt_pages(dkey, v0, 2**32 - 1, t(pages))
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=v0, pid0=2**32 - 1))
+        with pytest.raises(ContractViolation):
+            pc.crypt_pages(dkey, 2**64 - 2 * 4096, 1, t(pages))  # range overflows u64
+
+
+class TestFullSize:
+    """BASELINE config 2/3 size (1 GiB) through size-independent properties."""
+
+    @pytest.mark.parametrize("rounds", [8, 12, 20])
+    def test_1gib_roundtrip_and_samples(self, dkey, rounds):
+        import torch
+
+        n = 262_144
+        g = torch.Generator(device="cuda").manual_seed(1)
+        pages = torch.randint(0, 256, (n, 4096), dtype=torch.uint8, device="cuda", generator=g)
+        ct = pc.crypt_pages(dkey, BASE, 1, pages, rounds=rounds)
+        back = pc.crypt_pages(dkey, BASE, 1, ct, rounds=rounds)
+        assert torch.equal(back, pages)
+        # keystream linearity: ct ^ pt is the keystream, = crypt(zero page)
+        idx = torch.tensor([0, 1, 4095, 131072, n - 1], device="cuda")
+        ks = (ct[idx] ^ pages[idx]).cpu().numpy()
+        for j, p in enumerate(idx.tolist()):
+            want = C.crypt_pages(KEY, None, None, np.zeros((1, 4096), np.uint8), rounds=rounds,
+                                 vaddr0=BASE + 4096 * p, pid0=1)
+            assert np.array_equal(ks[j], want[0])
+        # a strided sample byte-exact against the oracle
+        sl = slice(0, n, 997)
+        sample_idx = np.arange(0, n, 997)
+        pv = BASE + 4096 * sample_idx.astype(np.uint64)
+        want = C.crypt_pages(KEY, pv, 1, pages[sl].cpu().numpy(), rounds=rounds, nthreads=8)
+        assert np.array_equal(ct[sl].cpu().numpy(), want)
+        del pages, ct, back
+        torch.cuda.empty_cache()
+
+
+class TestHostPath:
+    @pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 2048, 2049, 10_000])
+    def test_pageable_numpy(self, dkey, n):
+        pages = rand_pages(n, 10 + n)
+        got = pc.crypt_pages(dkey, BASE, 3, pages)
+        assert np.array_equal(got, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=3, nthreads=8))
+
+    @pytest.mark.parametrize("n", [1, 64, 9000])
+    def test_pinned_torch(self, dkey, n):
+        import torch
+
+        pages = rand_pages(n, 20 + n)
+        src = torch.from_numpy(pages).pin_memory()
+        dst = torch.empty_like(src).pin_memory()
+        pc.crypt_pages(dkey, BASE, 4, src, out=dst)
+        assert np.array_equal(dst.numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=4, nthreads=8))
+
+    def test_raw_key_host_with_descriptors(self, ref_pages):
+        r = ref_pages
+        got = pc.crypt_pages(r["key"].tobytes(), r["vaddrs"], r["pids"], r["pages"])
+        assert np.array_equal(got, r["ct"])
+        big = np.concatenate([r["pages"]] * 40)  # 2560 pages -> large path with descriptors
+        va = np.concatenate([r["vaddrs"]] * 40)
+        pi = np.concatenate([r["pids"]] * 40)
+        got = pc.crypt_pages(r["key"].tobytes(), va, pi, big)
+        assert np.array_equal(got, np.concatenate([r["ct"]] * 40))
+
+    def test_in_place_host(self, dkey):
+        pages = rand_pages(3000, 7)
+        buf = pages.copy()
+        pc.crypt_pages(dkey, BASE, 5, buf, out=buf)
+        assert np.array_equal(buf, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=5, nthreads=8))
+
+    def test_engine_stream_configs_agree(self, dkey):
+        pages = rand_pages(5000, 8)
+        want = C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=6, nthreads=8)
+        for ns, chunk in ((1, 512), (3, 777), (8, 4096)):
+            eng = pc.Engine(0, n_streams=ns, chunk_pages=chunk)
+            try:
+                got = pc.crypt_pages(dkey, BASE, 6, pages, engine=eng)
+                assert np.array_equal(got, want), (ns, chunk)
+            finally:
+                eng.destroy()
+
+
+class TestKeys:
+    def test_generate_distinct_and_roundtrip(self, cuda):
+        import torch
+
+        pages = rand_pages(16, 9)
+        a, b = pc.DeviceKey.generate(0), pc.DeviceKey.generate(0)
+        try:
+            ca = pc.crypt_pages(a, BASE, 1, t(pages))
+            cb = pc.crypt_pages(b, BASE, 1, t(pages))
+            assert not torch.equal(ca, cb)
+            assert np.array_equal(pc.crypt_pages(a, BASE, 1, ca).cpu().numpy(), pages)
+            assert pc.crypt_page(a, BASE, 1, pages[0].tobytes()) == ca[0].cpu().numpy().tobytes()
+        finally:
+            a.destroy()
+            b.destroy()
+
+    def test_destroy_is_idempotent_and_final(self, cuda):
+        k = pc.DeviceKey.install(KEY, 0)
+        k.destroy()
+        k.destroy()
+        assert k.destroyed
+        with pytest.raises(PageCryptError):
+            pc.crypt_pages(k, BASE, 1, rand_pages(1))
+
+    def test_device_key_matches_raw_key(self, dkey):
+        page = rand_pages(1, 12)[0].tobytes()
+        assert pc.crypt_page(dkey, BASE, 9, page) == pc.crypt_page(KEY, BASE, 9, page)
+
+
+class TestMultiDevice:
+    def test_partition_over_engines_is_identical(self, cuda):
+        import torch
+
+        ndev = torch.cuda.device_count()
+        devs = [d % ndev for d in range(max(2, ndev))]  # >= 2 slots even on one GPU
+        engines = [pc.Engine(d, n_streams=2, chunk_pages=1024) for d in devs]
+        keys = [pc.DeviceKey.install(KEY, d) for d in devs]
+        try:
+            pages = rand_pages(7001, 13)
+            got = partition.crypt_pages_multi(keys, engines, BASE, 11, pages)
+            assert np.array_equal(got, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=11, nthreads=8))
+            va = BASE + 4096 * np.random.default_rng(0).permutation(7001).astype(np.uint64)
+            got = partition.crypt_pages_multi(keys, engines, va, 11, pages)
+            assert np.array_equal(got, C.crypt_pages(KEY, va, 11, pages, nthreads=8))
+        finally:
+            for k in keys:
+                k.destroy()
+            for e in engines:
+                e.destroy()
