@@ -121,11 +121,18 @@ int pc_host_free(void *p);
 int pc_host_register(void *p, size_t bytes);
 int pc_host_unregister(void *p);
 
-/* ---- measurement ------------------------------------------------------- */
+/* ---- measurement and tuning ------------------------------------------- */
 /* Integer-pipe microbenchmark used for the roofline denominator: runs `kind`
- * (0 = LOP3 chains, 1 = IADD chains, 2 = IMAD chains, 3 = SHF rotates,
- * 4 = ChaCha-like ARX mix) on `device` and returns measured int32 lane-ops/s. */
+ * on `device` and returns measured int32 lane-ops/s.  0 = LOP3, 1 = IADD,
+ * 2 = IMAD, 3 = SHF rotate, 4 = ChaCha quarter rounds (12 ops each) as ptxas
+ * schedules them, 5 = quarter rounds with one rotate on the FMA pipe,
+ * 6 = IMAD.HI, 7 = IMAD.WIDE(+LOP3). */
 int pc_intpeak(int device, int kind, double *ops_per_s);
+/* Process-wide knobs: "rotmask" (compiled FMA-pipe rotate pattern of the
+ * crypt kernel, see chacha.cuh), "small_mode" (0 staged copies / 1 zero-copy
+ * for small host batches); pc_tune_get also reads "small_max". */
+int pc_tune(const char *knob, int64_t value);
+int pc_tune_get(const char *knob, int64_t *value);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,8 @@ SIGNATURES = {
     "pc_host_register": (c_int, [c_void_p, c_size_t]),
     "pc_host_unregister": (c_int, [c_void_p]),
     "pc_intpeak": (c_int, [c_int, c_int, P(ctypes.c_double)]),
+    "pc_tune": (c_int, [ctypes.c_char_p, ctypes.c_int64]),
+    "pc_tune_get": (c_int, [ctypes.c_char_p, P(ctypes.c_int64)]),
 }
 
 _lib = None
@@ -92,6 +94,16 @@ def check(rc: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args))
+
+
+def tune(knob: str, value: int) -> None:
+    call("pc_tune", knob.encode(), int(value))
+
+
+def tune_get(knob: str) -> int:
+    v = ctypes.c_int64()
+    call("pc_tune_get", knob.encode(), ctypes.byref(v))
+    return v.value
 
 
 def device_count() -> int:

@@ -55,10 +55,10 @@ __device__ __forceinline__ void page_seed(const PageDesc &d, uint64_t page, uint
 // v1: one thread = one 64-byte block.  The thread XORs its keystream into the
 // page bytes with four 16-byte loads/stores; a warp covers 2 KiB (half a page)
 // contiguously, sectors shared between the 4 loads of a thread hit L1.
-template <int ROUNDS, int AM>
+template <int ROUNDS, uint32_t MASK>
 __global__ void __launch_bounds__(256)
 k_crypt_blocks(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
-               uint64_t n_blocks, uint32_t one) {
+               uint64_t n_blocks, RotMul rm) {
   const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= n_blocks) return;
   uint32_t k[8], s[4];
@@ -68,13 +68,96 @@ k_crypt_blocks(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in,
   const uint4 *src = in + g * 4;
   uint4 d0 = ld_v4(src), d1 = ld_v4(src + 1), d2 = ld_v4(src + 2), d3 = ld_v4(src + 3);
   uint32_t x[16];
-  chacha_block<ROUNDS, AM>(x, k, s, one);
+  chacha_block<ROUNDS, MASK>(x, k, s, rm);
   d0.x ^= x[0];  d0.y ^= x[1];  d0.z ^= x[2];  d0.w ^= x[3];
   d1.x ^= x[4];  d1.y ^= x[5];  d1.z ^= x[6];  d1.w ^= x[7];
   d2.x ^= x[8];  d2.y ^= x[9];  d2.z ^= x[10]; d2.w ^= x[11];
   d3.x ^= x[12]; d3.y ^= x[13]; d3.z ^= x[14]; d3.w ^= x[15];
   uint4 *dst = out + g * 4;
   st_v4(dst, d0); st_v4(dst + 1, d1); st_v4(dst + 2, d2); st_v4(dst + 3, d3);
+}
+
+// ---------------------------------------------------------------------------
+// v2: persistent page-slot kernel.  A CTA of 256 threads owns 4 page slots;
+// thread t always handles block b = t % 64 of its slot's page and strides over
+// pages (page += 4 * gridDim.x), so per thread:
+//   * the first column quarter round of state column 3 -- words
+//     (sigma3, k3, k7, b), the only column holding the block index -- depends
+//     on (key, b) alone and is computed once per thread;
+//   * column rounds 1 and 2 -- (sigma1, k1, k5, vaddr_hi) and
+//     (sigma2, k2, k6, pid) -- are recomputed only when vaddr_hi or pid
+//     changes (warp-uniform test: a warp covers 32 blocks of one page);
+//   * only column 0 (sigma0, k0, k4, vaddr_lo) is recomputed for every page.
+// That is 3 of the 80 ChaCha20 quarter rounds per block (3 of 32 for ChaCha8)
+// hoisted out of the page loop; the result is bit-identical because the block
+// function is unchanged, only common subexpressions are shared.  The next
+// page's 64 bytes are loaded into registers before the current page's
+// rounds run (software pipelining), so HBM latency overlaps ARX work.
+template <int ROUNDS>
+__global__ void __launch_bounds__(256, 2)
+k_crypt_pages(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
+              uint64_t n_pages) {
+  constexpr RotMul rm{};
+  const uint32_t b = threadIdx.x & 63;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 4;
+  uint64_t page = static_cast<uint64_t>(blockIdx.x) * 4 + (threadIdx.x >> 6);
+  if (page >= n_pages) return;
+  uint32_t k[8];
+  load_key(key, k);
+  // column 3 after the first column quarter round: (key, b) only
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  // columns 1, 2 cache, keyed by (vaddr_hi, pid)
+  uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
+  uint32_t cached_hi = 0, cached_pid = 0;
+  bool cached = false;
+
+  const uint4 *src = in + page * 256 + b * 4;
+  uint4 d0 = ld_v4(src), d1 = ld_v4(src + 1), d2 = ld_v4(src + 2), d3 = ld_v4(src + 3);
+  for (;;) {
+    const uint64_t next = page + stride;
+    const bool has_next = next < n_pages;
+    uint4 n0, n1, n2, n3;
+    if (has_next) {
+      const uint4 *ns = in + next * 256 + b * 4;
+      n0 = ld_v4(ns); n1 = ld_v4(ns + 1); n2 = ld_v4(ns + 2); n3 = ld_v4(ns + 3);
+    }
+    uint32_t s[4];
+    page_seed(desc, page, s);
+    if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+      cached_hi = s[1];
+      cached_pid = s[2];
+      cached = true;
+    }
+    uint32_t x[16];
+    x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
+    quarter_round<0>(x[0], x[4], x[8], x[12], rm);
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int i = 1; i < ROUNDS / 2; ++i) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    uint4 *dst = out + page * 256 + b * 4;
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]),
+                              d3.w ^ (x[15] + b)));
+    if (!has_next) break;
+    page = next;
+    d0 = n0; d1 = n1; d2 = n2; d3 = n3;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -91,7 +174,7 @@ k_keystream_seeds(const uint32_t *__restrict__ key, const uint32_t *__restrict__
   load_key(key, k);
   const uint4 sv = __ldg(reinterpret_cast<const uint4 *>(seeds) + i);
   s[0] = sv.x; s[1] = sv.y; s[2] = sv.z; s[3] = sv.w;
-  chacha_block<ROUNDS, kAddAlu>(x, k, s, 1u);
+  chacha_block<ROUNDS, 0>(x, k, s, RotMul{});
   uint4 *o = reinterpret_cast<uint4 *>(out) + i * 4;
   o[0] = make_uint4(x[0], x[1], x[2], x[3]);
   o[1] = make_uint4(x[4], x[5], x[6], x[7]);
@@ -113,7 +196,7 @@ __global__ void k_keygen(const uint32_t *__restrict__ entropy, uint32_t *__restr
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   s[0] = static_cast<uint32_t>(t); s[1] = static_cast<uint32_t>(t >> 32);
   s[2] = static_cast<uint32_t>(c) ^ (smid << 24); s[3] = static_cast<uint32_t>(c >> 32);
-  chacha_block<20, kAddAlu>(x, k, s, 1u);
+  chacha_block<20, 0>(x, k, s, RotMul{});
 #pragma unroll
   for (int i = 0; i < 8; ++i) key_out[i] = x[i];
 }
@@ -121,36 +204,48 @@ __global__ void k_keygen(const uint32_t *__restrict__ entropy, uint32_t *__restr
 // ---------------------------------------------------------------------------
 // Integer-pipe microbenchmarks (roofline denominators, pc_intpeak).  Eight
 // independent chains per thread so issue, not latency, bounds them.
+//   0 LOP3   1 IADD (ptxas fuses pairs into IADD3)   2 IMAD   3 SHF rotate
+//   4 ChaCha quarter rounds as ptxas schedules them (adds on IMAD)
+//   5 quarter rounds with the rotate by 7 on the FMA pipe (ROTMASK nibble 8)
+//   6 IMAD.HI   7 IMAD.WIDE
 template <int KIND>
 __global__ void __launch_bounds__(256)
-k_intpeak(uint32_t seed, uint32_t one, int iters, uint32_t *sink) {
+k_intpeak(uint32_t seed, RotMul rm, int iters, uint32_t *sink) {
   uint32_t v[8], w[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) { v[j] = seed ^ (threadIdx.x * 0x9e3779b9u + j); w[j] = v[j] * 3u + j; }
   for (int it = 0; it < iters; ++it) {
+    if constexpr (KIND <= 3 || KIND >= 6) {
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+      for (int r = 0; r < 16; ++r) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if constexpr (KIND == 0) { // LOP3
-          asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[j]) : "r"(w[j]), "r"(v[(j + 1) & 7]));
-        } else if constexpr (KIND == 1) { // IADD
-          asm volatile("add.u32 %0, %0, %1;" : "+r"(v[j]) : "r"(w[j]));
-        } else if constexpr (KIND == 2) { // IMAD
-          asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(v[j]) : "r"(one), "r"(w[j]));
-        } else if constexpr (KIND == 3) { // SHF rotate
-          asm volatile("shf.l.wrap.b32 %0, %0, %0, 7;" : "+r"(v[j]));
+        for (int j = 0; j < 8; ++j) {
+          if constexpr (KIND == 0) {
+            asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[j]) : "r"(w[j]), "r"(v[(j + 1) & 7]));
+          } else if constexpr (KIND == 1) {
+            asm volatile("add.u32 %0, %0, %1;" : "+r"(v[j]) : "r"(w[j]));
+          } else if constexpr (KIND == 2) {
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(v[j]) : "r"(rm.m16), "r"(w[j]));
+          } else if constexpr (KIND == 3) {
+            asm volatile("shf.l.wrap.b32 %0, %0, %0, 7;" : "+r"(v[j]));
+          } else if constexpr (KIND == 6) {
+            asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(v[j]) : "r"(rm.m12), "r"(w[j]));
+          } else {
+            uint64_t p;
+            asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(v[j]), "r"(rm.m12));
+            v[j] = static_cast<uint32_t>(p) ^ static_cast<uint32_t>(p >> 32);
+          }
         }
       }
-    }
-    if constexpr (KIND == 4 || KIND == 5) {
-      // ChaCha ARX: two independent quarter-round states per thread.
+    } else {
+      // two independent ChaCha states per thread (v, w), 16 quarter rounds
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        quarter_round<KIND == 4 ? kAddAlu : kAddSplitA>(v[0], v[1], v[2], v[3], one);
-        quarter_round<KIND == 4 ? kAddAlu : kAddSplitA>(v[4], v[5], v[6], v[7], one);
-        quarter_round<KIND == 4 ? kAddAlu : kAddSplitA>(w[0], w[1], w[2], w[3], one);
-        quarter_round<KIND == 4 ? kAddAlu : kAddSplitA>(w[4], w[5], w[6], w[7], one);
+        constexpr uint32_t N = KIND == 4 ? 0u : 8u;
+        quarter_round<N>(v[0], v[1], v[2], v[3], rm);
+        quarter_round<N>(v[4], v[5], v[6], v[7], rm);
+        quarter_round<N>(w[0], w[1], w[2], w[3], rm);
+        quarter_round<N>(w[4], w[5], w[6], w[7], rm);
       }
     }
   }

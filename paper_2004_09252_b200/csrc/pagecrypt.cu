@@ -73,42 +73,102 @@ int env_int(const char *name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
-// Tuning knobs (fixed at first use; env overrides are for measurement).
+// Tuning knobs (env defaults at first use, pc_tune() at run time).
 struct Tuning {
-  int add_mode;    // pc::AddMode for the crypt kernel
-  int small_mode;  // 0 = staged copies, 1 = zero-copy on mapped pinned memory
-  size_t small_max;
+  std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
+  std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
+  std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
+  std::atomic<int> kernel{2};          // 1 = k_crypt_blocks (thread per block), 2 = k_crypt_pages (persistent)
+  std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
+  Tuning() {
+    kernel = env_int("PAGECRYPT_KERNEL", 2);
+    ctas_per_sm = env_int("PAGECRYPT_CTAS_PER_SM", 0);
+    if (const char *v = std::getenv("PAGECRYPT_ROTMASK")) rot_mask = static_cast<uint32_t>(std::strtoul(v, nullptr, 0));
+    small_mode = env_int("PAGECRYPT_SMALL_MODE", 1);
+    small_max = static_cast<size_t>(env_int("PAGECRYPT_SMALL_MAX", 64));
+  }
 };
-const Tuning &tuning() {
-  static const Tuning t = {env_int("PAGECRYPT_ADDMODE", pc::kAddAlu),
-                           env_int("PAGECRYPT_SMALL_MODE", 1),
-                           static_cast<size_t>(env_int("PAGECRYPT_SMALL_MAX", 64))};
+Tuning &tuning() {
+  static Tuning t;
   return t;
 }
 
-template <int R>
-void launch_crypt_r(int am, const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
-                    uint64_t n_blocks, cudaStream_t st) {
+// Compiled ROTMASK variants of k_crypt_blocks (chacha.cuh): FMA-pipe rotates
+// per double round.  Measured on B200 (profiles/r01_rotmask_sweep.txt): no
+// variant beats 0 -- IMAD.HI is half rate and adds dispatch stalls -- so 0 is
+// the default and the others stay for the record.
+constexpr uint32_t kRotMasks[] = {0x00000000u, 0x88888888u, 0x888888AAu, 0x88888AAAu,
+                                  0xAAAA8888u, 0xAAAAAAAAu};
+
+constexpr pc::RotMul kRotMul{1u << 16, 1u << 12, 1u << 8, 1u << 7};
+
+template <int R, uint32_t M>
+void launch_crypt_rm(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
+                     uint64_t n_blocks, cudaStream_t st) {
   const dim3 block(256);
   const dim3 grid(static_cast<unsigned>((n_blocks + 255) / 256));
-  auto i4 = static_cast<const uint4 *>(in);
-  auto o4 = static_cast<uint4 *>(out);
-  switch (am) {
-    case pc::kAddFma: pc::k_crypt_blocks<R, pc::kAddFma><<<grid, block, 0, st>>>(key, d, i4, o4, n_blocks, 1u); break;
-    case pc::kAddSplitA: pc::k_crypt_blocks<R, pc::kAddSplitA><<<grid, block, 0, st>>>(key, d, i4, o4, n_blocks, 1u); break;
-    default: pc::k_crypt_blocks<R, pc::kAddAlu><<<grid, block, 0, st>>>(key, d, i4, o4, n_blocks, 1u); break;
+  pc::k_crypt_blocks<R, M><<<grid, block, 0, st>>>(key, d, static_cast<const uint4 *>(in),
+                                                   static_cast<uint4 *>(out), n_blocks, kRotMul);
+}
+
+template <int R>
+void launch_crypt_r(uint32_t mask, const uint32_t *key, const pc::PageDesc &d, const void *in,
+                    void *out, uint64_t n_blocks, cudaStream_t st) {
+  switch (mask) {
+    case 0x88888888u: launch_crypt_rm<R, 0x88888888u>(key, d, in, out, n_blocks, st); break;
+    case 0x888888AAu: launch_crypt_rm<R, 0x888888AAu>(key, d, in, out, n_blocks, st); break;
+    case 0x88888AAAu: launch_crypt_rm<R, 0x88888AAAu>(key, d, in, out, n_blocks, st); break;
+    case 0xAAAA8888u: launch_crypt_rm<R, 0xAAAA8888u>(key, d, in, out, n_blocks, st); break;
+    case 0xAAAAAAAAu: launch_crypt_rm<R, 0xAAAAAAAAu>(key, d, in, out, n_blocks, st); break;
+    default: launch_crypt_rm<R, 0u>(key, d, in, out, n_blocks, st); break;
   }
+}
+
+// Persistent grid for k_crypt_pages: SMs x resident CTAs (occupancy), capped
+// by the number of 4-page slots.
+template <int R>
+unsigned pages_grid(size_t n_pages) {
+  static int sms[64] = {0}, occ[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!sms[dev]) {
+    cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
+    occ[dev] = o > 0 ? o : 1;
+  }
+  const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : occ[dev];
+  const uint64_t want = static_cast<uint64_t>(sms[dev]) * per_sm;
+  const uint64_t slots = (n_pages + 3) / 4;
+  return static_cast<unsigned>(std::min<uint64_t>(want, slots));
+}
+
+template <int R>
+void launch_pages_r(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
+                    size_t n_pages, cudaStream_t st) {
+  pc::k_crypt_pages<R><<<pages_grid<R>(n_pages), 256, 0, st>>>(
+      key, d, static_cast<const uint4 *>(in), static_cast<uint4 *>(out), n_pages);
 }
 
 int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
                  size_t n_pages, int rounds, cudaStream_t st) {
   if (n_pages == 0) return PC_OK;
+  if (tuning().kernel.load() == 2) {
+    switch (rounds) {
+      case 8: launch_pages_r<8>(key, d, in, out, n_pages, st); break;
+      case 12: launch_pages_r<12>(key, d, in, out, n_pages, st); break;
+      default: launch_pages_r<20>(key, d, in, out, n_pages, st); break;
+    }
+    CU(cudaGetLastError());
+    return PC_OK;
+  }
   const uint64_t n_blocks = static_cast<uint64_t>(n_pages) * PC_BLOCKS_PER_PAGE;
-  const int am = tuning().add_mode;
+  const uint32_t mask = tuning().rot_mask.load(std::memory_order_relaxed);
   switch (rounds) {
-    case 8: launch_crypt_r<8>(am, key, d, in, out, n_blocks, st); break;
-    case 12: launch_crypt_r<12>(am, key, d, in, out, n_blocks, st); break;
-    default: launch_crypt_r<20>(am, key, d, in, out, n_blocks, st); break;
+    case 8: launch_crypt_r<8>(mask, key, d, in, out, n_blocks, st); break;
+    case 12: launch_crypt_r<12>(mask, key, d, in, out, n_blocks, st); break;
+    default: launch_crypt_r<20>(mask, key, d, in, out, n_blocks, st); break;
   }
   CU(cudaGetLastError());
   return PC_OK;
@@ -404,7 +464,7 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
   }
   CUE(cudaHostAlloc(&e->h_key, 256, cudaHostAllocDefault));
   CUE(cudaMalloc(&e->d_rawkey, 256));
-  const size_t sm = tuning().small_max;
+  const size_t sm = tuning().small_max.load();
   e->small_bytes = 256 + sm * 16 + sm * PC_PAGE_SIZE;
   CUE(cudaHostAlloc(&e->h_small, e->small_bytes, cudaHostAllocMapped));
   CUE(cudaHostGetDevicePointer(reinterpret_cast<void **>(&e->hd_small), e->h_small, 0));
@@ -637,7 +697,7 @@ int pc_host_unregister(void *p) {
 // ---- measurement -------------------------------------------------------------
 int pc_intpeak(int device, int kind, double *ops_per_s) {
   if (!ops_per_s) return fail(PC_EINVAL, "ops_per_s is NULL");
-  if (kind < 0 || kind > 5) return fail(PC_EINVAL, "kind must be 0..5");
+  if (kind < 0 || kind > 7) return fail(PC_EINVAL, "kind must be 0..7");
   DeviceGuard g(device);
   CU(g.err);
   int sms = 0;
@@ -645,15 +705,18 @@ int pc_intpeak(int device, int kind, double *ops_per_s) {
   uint32_t *sink = nullptr;
   CU(cudaMalloc(&sink, 1024 * 4));
   const dim3 grid(sms * 8), block(256);
-  const int iters = kind >= 4 ? 1000 : 1500;
+  const bool arx = kind == 4 || kind == 5;
+  const int iters = arx ? 1000 : 1500;
   auto run = [&](int it) {
     switch (kind) {
-      case 0: pc::k_intpeak<0><<<grid, block>>>(1u, 1u, it, sink); break;
-      case 1: pc::k_intpeak<1><<<grid, block>>>(1u, 1u, it, sink); break;
-      case 2: pc::k_intpeak<2><<<grid, block>>>(1u, 1u, it, sink); break;
-      case 3: pc::k_intpeak<3><<<grid, block>>>(1u, 1u, it, sink); break;
-      case 4: pc::k_intpeak<4><<<grid, block>>>(1u, 1u, it, sink); break;
-      default: pc::k_intpeak<5><<<grid, block>>>(1u, 1u, it, sink); break;
+      case 0: pc::k_intpeak<0><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 1: pc::k_intpeak<1><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 2: pc::k_intpeak<2><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 3: pc::k_intpeak<3><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 4: pc::k_intpeak<4><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 5: pc::k_intpeak<5><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 6: pc::k_intpeak<6><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      default: pc::k_intpeak<7><<<grid, block>>>(1u, kRotMul, it, sink); break;
     }
   };
   cudaEvent_t a, b;
@@ -674,8 +737,52 @@ int pc_intpeak(int device, int kind, double *ops_per_s) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(sink);
-  const double ops_per_iter = kind >= 4 ? 16.0 * 12.0 : 16.0 * 8.0;
+  // ops per iteration: ARX = 16 quarter rounds x 12 ops (op-count convention,
+  // independent of how many instructions implement them); others 16 x 8 chains
+  // (kind 7 counts IMAD.WIDE + its LOP3 as 2 ops).
+  const double ops_per_iter = arx ? 16.0 * 12.0 : (kind == 7 ? 16.0 * 8.0 * 2.0 : 16.0 * 8.0);
   *ops_per_s = static_cast<double>(grid.x) * block.x * iters * ops_per_iter / (best_ms * 1e-3);
+  return PC_OK;
+}
+
+int pc_tune(const char *knob, int64_t value) {
+  if (!knob) return fail(PC_EINVAL, "knob is NULL");
+  Tuning &t = tuning();
+  if (!std::strcmp(knob, "rotmask")) {
+    for (uint32_t m : kRotMasks)
+      if (static_cast<int64_t>(m) == value) {
+        t.rot_mask = m;
+        return PC_OK;
+      }
+    return fail(PC_EINVAL, "rotmask %#llx is not a compiled variant", (unsigned long long)value);
+  }
+  if (!std::strcmp(knob, "small_mode")) {
+    if (value != 0 && value != 1) return fail(PC_EINVAL, "small_mode must be 0 or 1");
+    t.small_mode = static_cast<int>(value);
+    return PC_OK;
+  }
+  if (!std::strcmp(knob, "kernel")) {
+    if (value != 1 && value != 2) return fail(PC_EINVAL, "kernel must be 1 or 2");
+    t.kernel = static_cast<int>(value);
+    return PC_OK;
+  }
+  if (!std::strcmp(knob, "ctas_per_sm")) {
+    if (value < 0 || value > 32) return fail(PC_EINVAL, "ctas_per_sm must be 0..32");
+    t.ctas_per_sm = static_cast<int>(value);
+    return PC_OK;
+  }
+  return fail(PC_EINVAL, "unknown knob '%s'", knob);
+}
+
+int pc_tune_get(const char *knob, int64_t *value) {
+  if (!knob || !value) return fail(PC_EINVAL, "NULL argument");
+  Tuning &t = tuning();
+  if (!std::strcmp(knob, "rotmask")) *value = t.rot_mask;
+  else if (!std::strcmp(knob, "small_mode")) *value = t.small_mode;
+  else if (!std::strcmp(knob, "small_max")) *value = static_cast<int64_t>(t.small_max.load());
+  else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
+  else if (!std::strcmp(knob, "ctas_per_sm")) *value = t.ctas_per_sm;
+  else return fail(PC_EINVAL, "unknown knob '%s'", knob);
   return PC_OK;
 }
 
