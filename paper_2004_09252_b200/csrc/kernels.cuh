@@ -161,6 +161,93 @@ k_crypt_pages(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, 
 }
 
 // ---------------------------------------------------------------------------
+// v3: the v2 page loop (same hoisting, same thread -> block index mapping) with
+// fully coalesced global traffic: each warp moves its half page (2 KiB) with
+// four 512-byte-contiguous LDG.128/STG.128 (lane l takes bytes 16l + 512j)
+// and exchanges it through 2 KiB of shared memory per warp, so that lane t
+// can XOR block t.  The 16-byte chunks are XOR-swizzled (chunk q of the tile
+// lives at column (q & 7) ^ ((q >> 3) & 7) of 128-byte row q >> 3), which
+// makes both the coalesced and the per-block LDS/STS.128 patterns
+// bank-conflict-free.  Used for pages in mapped pinned host memory (zero-copy:
+// every PCIe request is a full 512-byte warp access) and selectable for HBM.
+__device__ __forceinline__ uint32_t swz(uint32_t q) { return (q & ~7u) | ((q ^ (q >> 3)) & 7u); }
+
+template <int ROUNDS>
+__global__ void __launch_bounds__(256, 2)
+k_crypt_pages_coalesced(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
+                        uint64_t n_pages) {
+  constexpr RotMul rm{};
+  __shared__ uint4 tile[8][128]; // one 2 KiB half page per warp
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t b = threadIdx.x & 63;       // block index within the page (constant)
+  const uint32_t half = (threadIdx.x >> 5) & 1;
+  uint4 *t = tile[warp];
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 4;
+  uint64_t page = static_cast<uint64_t>(blockIdx.x) * 4 + (threadIdx.x >> 6);
+  if (page >= n_pages) return;
+  uint32_t k[8];
+  load_key(key, k);
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
+  uint32_t cached_hi = 0, cached_pid = 0;
+  bool cached = false;
+
+  // coalesced: lane l of load j takes tile chunk q = 32j + l
+  const uint4 *src = in + page * 256 + half * 128 + lane;
+  uint4 d0 = ld_v4(src), d1 = ld_v4(src + 32), d2 = ld_v4(src + 64), d3 = ld_v4(src + 96);
+  for (;;) {
+    const uint64_t next = page + stride;
+    const bool has_next = next < n_pages;
+    // stage this half page into shared memory (swizzled), then prefetch the next
+    t[swz(lane)] = d0; t[swz(lane + 32)] = d1; t[swz(lane + 64)] = d2; t[swz(lane + 96)] = d3;
+    if (has_next) {
+      const uint4 *ns = in + next * 256 + half * 128 + lane;
+      d0 = ld_v4(ns); d1 = ld_v4(ns + 32); d2 = ld_v4(ns + 64); d3 = ld_v4(ns + 96);
+    }
+    uint32_t s[4];
+    page_seed(desc, page, s);
+    if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+      cached_hi = s[1];
+      cached_pid = s[2];
+      cached = true;
+    }
+    uint32_t x[16];
+    x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
+    quarter_round<0>(x[0], x[4], x[8], x[12], rm);
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int i = 1; i < ROUNDS / 2; ++i) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    __syncwarp();
+    // lane owns tile chunks 4*lane .. 4*lane+3 (its 64-byte block)
+    const uint32_t q = 4 * lane;
+    uint4 v0 = t[swz(q)], v1 = t[swz(q + 1)], v2 = t[swz(q + 2)], v3 = t[swz(q + 3)];
+    v0.x ^= x[0] + kSigma0; v0.y ^= x[1] + kSigma1; v0.z ^= x[2] + kSigma2; v0.w ^= x[3] + kSigma3;
+    v1.x ^= x[4] + k[0]; v1.y ^= x[5] + k[1]; v1.z ^= x[6] + k[2]; v1.w ^= x[7] + k[3];
+    v2.x ^= x[8] + k[4]; v2.y ^= x[9] + k[5]; v2.z ^= x[10] + k[6]; v2.w ^= x[11] + k[7];
+    v3.x ^= x[12] + s[0]; v3.y ^= x[13] + s[1]; v3.z ^= x[14] + s[2]; v3.w ^= x[15] + b;
+    t[swz(q)] = v0; t[swz(q + 1)] = v1; t[swz(q + 2)] = v2; t[swz(q + 3)] = v3;
+    __syncwarp();
+    uint4 *dst = out + page * 256 + half * 128 + lane;
+    st_v4(dst, t[swz(lane)]); st_v4(dst + 32, t[swz(lane + 32)]);
+    st_v4(dst + 64, t[swz(lane + 64)]); st_v4(dst + 96, t[swz(lane + 96)]);
+    __syncwarp();
+    if (!has_next) break;
+    page = next;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Keystream only, arbitrary seeds: seeds[4*i .. 4*i+3] are state words 12..15
 // of block i; out[16*i ..] its 16 keystream words (block-major, like
 // _chacha_numba.keystream_words, _chacha_numba.py:45-50).

@@ -78,10 +78,13 @@ struct Tuning {
   std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
   std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
-  std::atomic<int> kernel{2};          // 1 = k_crypt_blocks (thread per block), 2 = k_crypt_pages (persistent)
+  std::atomic<int> kernel{2};          // HBM kernel: 1 = k_crypt_blocks, 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced
+  std::atomic<int> host_mode{2};       // large host batches: 0 = round-robin streams, 1 = zero-copy kernel
+                                       // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams
   std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
   Tuning() {
     kernel = env_int("PAGECRYPT_KERNEL", 2);
+    host_mode = env_int("PAGECRYPT_HOST_MODE", 2);
     ctas_per_sm = env_int("PAGECRYPT_CTAS_PER_SM", 0);
     if (const char *v = std::getenv("PAGECRYPT_ROTMASK")) rot_mask = static_cast<uint32_t>(std::strtoul(v, nullptr, 0));
     small_mode = env_int("PAGECRYPT_SMALL_MODE", 1);
@@ -126,7 +129,7 @@ void launch_crypt_r(uint32_t mask, const uint32_t *key, const pc::PageDesc &d, c
 
 // Persistent grid for k_crypt_pages: SMs x resident CTAs (occupancy), capped
 // by the number of 4-page slots.
-template <int R>
+template <int R, bool Coalesced>
 unsigned pages_grid(size_t n_pages) {
   static int sms[64] = {0}, occ[64] = {0};
   int dev = 0;
@@ -135,7 +138,10 @@ unsigned pages_grid(size_t n_pages) {
   if (!sms[dev]) {
     cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
     int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
+    if constexpr (Coalesced)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
     occ[dev] = o > 0 ? o : 1;
   }
   const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : occ[dev];
@@ -145,20 +151,27 @@ unsigned pages_grid(size_t n_pages) {
 }
 
 template <int R>
-void launch_pages_r(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
-                    size_t n_pages, cudaStream_t st) {
-  pc::k_crypt_pages<R><<<pages_grid<R>(n_pages), 256, 0, st>>>(
-      key, d, static_cast<const uint4 *>(in), static_cast<uint4 *>(out), n_pages);
+void launch_pages_r(bool coalesced, const uint32_t *key, const pc::PageDesc &d, const void *in,
+                    void *out, size_t n_pages, cudaStream_t st) {
+  auto i4 = static_cast<const uint4 *>(in);
+  auto o4 = static_cast<uint4 *>(out);
+  if (coalesced)
+    pc::k_crypt_pages_coalesced<R><<<pages_grid<R, true>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
+  else
+    pc::k_crypt_pages<R><<<pages_grid<R, false>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
 }
 
+// kernel_override: 0 = the "kernel" knob, else force 1/2/3 (the zero-copy
+// host path forces 3).
 int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
-                 size_t n_pages, int rounds, cudaStream_t st) {
+                 size_t n_pages, int rounds, cudaStream_t st, int kernel_override = 0) {
   if (n_pages == 0) return PC_OK;
-  if (tuning().kernel.load() == 2) {
+  const int kern = kernel_override ? kernel_override : tuning().kernel.load();
+  if (kern == 2 || kern == 3) {
     switch (rounds) {
-      case 8: launch_pages_r<8>(key, d, in, out, n_pages, st); break;
-      case 12: launch_pages_r<12>(key, d, in, out, n_pages, st); break;
-      default: launch_pages_r<20>(key, d, in, out, n_pages, st); break;
+      case 8: launch_pages_r<8>(kern == 3, key, d, in, out, n_pages, st); break;
+      case 12: launch_pages_r<12>(kern == 3, key, d, in, out, n_pages, st); break;
+      default: launch_pages_r<20>(kern == 3, key, d, in, out, n_pages, st); break;
     }
     CU(cudaGetLastError());
     return PC_OK;
@@ -271,7 +284,9 @@ struct pc_engine {
   size_t chunk_pages = 0;
   std::mutex mu;
   std::vector<cudaStream_t> streams;
-  std::vector<cudaEvent_t> done;
+  std::vector<cudaEvent_t> done;    // slot's D2H complete
+  std::vector<cudaEvent_t> ev_h2d;  // slot's H2D complete (host_mode 2)
+  std::vector<cudaEvent_t> ev_k;    // slot's kernel complete (host_mode 2)
   std::vector<uint8_t *> d_pages;   // per-stream device staging, chunk_pages*4096
   std::vector<uint64_t *> d_vaddrs; // per-stream descriptor staging
   std::vector<uint32_t *> d_pids;
@@ -429,7 +444,7 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
   *out = nullptr;
   if (n_streams <= 0) n_streams = 4;
   if (n_streams > 16) n_streams = 16;
-  if (chunk_pages == 0) chunk_pages = 2048; // 8 MiB per stage
+  if (chunk_pages == 0) chunk_pages = 8192; // 32 MiB per stage
   DeviceGuard g(device);
   CU(g.err);
   auto *e = new pc_engine();
@@ -449,6 +464,8 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
   } while (0)
   e->streams.assign(n_streams, nullptr);
   e->done.assign(n_streams, nullptr);
+  e->ev_h2d.assign(n_streams, nullptr);
+  e->ev_k.assign(n_streams, nullptr);
   e->d_pages.assign(n_streams, nullptr);
   e->d_vaddrs.assign(n_streams, nullptr);
   e->d_pids.assign(n_streams, nullptr);
@@ -457,6 +474,8 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
   for (int s = 0; s < n_streams; ++s) {
     CUE(cudaStreamCreateWithFlags(&e->streams[s], cudaStreamNonBlocking));
     CUE(cudaEventCreateWithFlags(&e->done[s], cudaEventDisableTiming));
+    CUE(cudaEventCreateWithFlags(&e->ev_h2d[s], cudaEventDisableTiming));
+    CUE(cudaEventCreateWithFlags(&e->ev_k[s], cudaEventDisableTiming));
     CUE(cudaMalloc(&e->d_pages[s], chunk_pages * PC_PAGE_SIZE));
     CUE(cudaMalloc(&e->d_vaddrs[s], chunk_pages * 8));
     CUE(cudaMalloc(&e->d_pids[s], chunk_pages * 4));
@@ -491,6 +510,8 @@ int pc_engine_destroy(pc_engine *e) {
     if (e->h_bounce[s]) cudaFreeHost(e->h_bounce[s]);
     if (e->h_desc[s]) cudaFreeHost(e->h_desc[s]);
     if (e->done[s]) cudaEventDestroy(e->done[s]);
+    if (e->ev_h2d[s]) cudaEventDestroy(e->ev_h2d[s]);
+    if (e->ev_k[s]) cudaEventDestroy(e->ev_k[s]);
     if (e->streams[s]) cudaStreamDestroy(e->streams[s]);
   }
   cudaGetLastError();
@@ -511,12 +532,15 @@ int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, cons
   const size_t off_pg = off_p + ((n * 4 + 255) & ~size_t(255));
   const size_t used = off_pg + n * PC_PAGE_SIZE;
   uint8_t *h = e->h_small;
+  cudaStream_t st = e->streams[0];
+  const bool zc = tuning().small_mode == 1;
+  // zero-copy straight on the caller's pages when they are pinned already
+  void *in_dev = nullptr, *out_dev = nullptr;
+  const bool direct = zc && pinned_alias(in, &in_dev) && pinned_alias(out, &out_dev);
   if (raw_key) std::memcpy(h, raw_key, 32);
   if (vaddrs) std::memcpy(h + off_v, vaddrs, n * 8);
   if (pids) std::memcpy(h + off_p, pids, n * 4);
-  std::memcpy(h + off_pg, in, n * PC_PAGE_SIZE);
-  cudaStream_t st = e->streams[0];
-  const bool zc = tuning().small_mode == 1;
+  if (!direct) std::memcpy(h + off_pg, in, n * PC_PAGE_SIZE);
   uint8_t *base = zc ? e->hd_small : e->d_small;
   const pc::PageDesc d{vaddrs ? reinterpret_cast<const uint64_t *>(base + off_v) : nullptr,
                        pids ? reinterpret_cast<const uint32_t *>(base + off_p) : nullptr, vaddr0, pid0};
@@ -524,7 +548,12 @@ int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, cons
   int rc = PC_OK;
   cudaError_t err = cudaSuccess;
   if (!zc) err = cudaMemcpyAsync(e->d_small, h, used, cudaMemcpyHostToDevice, st);
-  if (err == cudaSuccess) rc = launch_crypt(key, d, base + off_pg, base + off_pg, n, rounds, st);
+  if (err == cudaSuccess) {
+    if (direct)
+      rc = launch_crypt(key, d, in_dev, out_dev, n, rounds, st, 3);
+    else
+      rc = launch_crypt(key, d, base + off_pg, base + off_pg, n, rounds, st, zc ? 3 : 0);
+  }
   if (err == cudaSuccess && rc == PC_OK && !zc)
     err = cudaMemcpyAsync(h + off_pg, e->d_small + off_pg, n * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, st);
   if (!zc && raw_key) {
@@ -536,7 +565,7 @@ int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, cons
   if (rc != PC_OK) return rc;
   if (err == cudaSuccess) err = e3;
   CU(err);
-  std::memcpy(out, h + off_pg, n * PC_PAGE_SIZE);
+  if (!direct) std::memcpy(out, h + off_pg, n * PC_PAGE_SIZE);
   return PC_OK;
 }
 
@@ -546,57 +575,113 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   const bool pin_in = pinned_alias(in, &in_dev);
   const bool pin_out = pinned_alias(out, &out_dev);
   const bool has_desc = vaddrs || pids;
+  if (tuning().host_mode.load() == 1 && pin_in && pin_out) {
+    // zero-copy: one coalesced kernel streams the pages over PCIe itself
+    // (GPU-initiated reads and posted writes, both directions at once)
+    void *v_dev = nullptr, *p_dev = nullptr;
+    const bool desc_ok = (!vaddrs || pinned_alias(vaddrs, &v_dev)) && (!pids || pinned_alias(pids, &p_dev));
+    if (desc_ok) {
+      const pc::PageDesc d{static_cast<const uint64_t *>(v_dev), static_cast<const uint32_t *>(p_dev),
+                           vaddr0, pid0};
+      int rc = launch_crypt(key, d, in_dev, out_dev, n, rounds, e->streams[0], 3);
+      if (rc != PC_OK) return rc;
+      CU(cudaStreamSynchronize(e->streams[0]));
+      return PC_OK;
+    }
+  }
+  // Staged pipeline over S device slots.  host_mode 2 (default): one H2D
+  // stream, one compute stream and one D2H stream chained by events, so each
+  // copy engine sees its transfers back to back; host_mode 0: chunk c runs
+  // H2D -> kernel -> D2H in order on stream c % S.
   const int S = e->n_streams;
   const size_t C = e->chunk_pages;
+  const bool dedicated = tuning().host_mode.load() == 2 && S >= 3;
   if (!pin_in || !pin_out) {
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(cudaHostAlloc(&e->h_bounce[s], C * PC_PAGE_SIZE, cudaHostAllocDefault));
   }
-  const size_t n_chunks = (n + C - 1) / C;
+  // Chunk schedule: ramp up C/8, C/4, C/2 at the start and down at the end
+  // (when the batch is large enough) so the pipeline fills and drains with
+  // small transfers while the steady state uses full C-page chunks.
+  std::vector<size_t> starts;
+  {
+    std::vector<size_t> sizes;
+    size_t left = n;
+    const size_t ramp[3] = {C / 8, C / 4, C / 2};
+    const bool do_ramp = C >= 64 && n >= 4 * C;
+    std::vector<size_t> tail;
+    if (do_ramp) {
+      for (size_t r : ramp) { sizes.push_back(r); left -= r; }
+      for (size_t r : ramp) { tail.push_back(r); left -= r; }
+    }
+    while (left > 0) {
+      const size_t m = std::min(C, left);
+      sizes.push_back(m);
+      left -= m;
+    }
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) sizes.push_back(*it);
+    size_t p = 0;
+    for (size_t m : sizes) { starts.push_back(p); p += m; }
+    starts.push_back(p);
+  }
+  const size_t n_chunks = starts.size() - 1;
   auto *src_b = static_cast<const uint8_t *>(in);
   auto *dst_b = static_cast<uint8_t *>(out);
-  auto finish = [&](size_t c) -> int { // chunk c's stream slot is about to be reused / drained
+  auto finish = [&](size_t c) -> int { // chunk c's slot is about to be reused / drained
     const int s = static_cast<int>(c % S);
     CU(cudaEventSynchronize(e->done[s]));
     if (!pin_out) {
-      const size_t p0 = c * C, m = std::min(C, n - p0);
+      const size_t p0 = starts[c], m = starts[c + 1] - p0;
       std::memcpy(dst_b + p0 * PC_PAGE_SIZE, e->h_bounce[s], m * PC_PAGE_SIZE);
     }
     return PC_OK;
   };
   for (size_t c = 0; c < n_chunks; ++c) {
     const int s = static_cast<int>(c % S);
-    cudaStream_t st = e->streams[s];
-    const size_t p0 = c * C, m = std::min(C, n - p0);
-    if (c >= static_cast<size_t>(S) && (!pin_in || !pin_out || has_desc)) {
-      int rc = finish(c - S);
-      if (rc != PC_OK) return rc;
+    cudaStream_t sh = dedicated ? e->streams[0] : e->streams[s];
+    cudaStream_t sk = dedicated ? e->streams[1] : e->streams[s];
+    cudaStream_t sd = dedicated ? e->streams[2] : e->streams[s];
+    const size_t p0 = starts[c], m = starts[c + 1] - p0;
+    if (c >= static_cast<size_t>(S)) {
+      if (!pin_in || !pin_out || has_desc) {
+        int rc = finish(c - S); // host reuses this slot's bounce / descriptor staging
+        if (rc != PC_OK) return rc;
+      } else if (dedicated) {
+        CU(cudaStreamWaitEvent(sh, e->done[s], 0)); // device slot free once its D2H is done
+      }
     }
     const uint8_t *src = src_b + p0 * PC_PAGE_SIZE;
     if (!pin_in) {
       std::memcpy(e->h_bounce[s], src, m * PC_PAGE_SIZE);
       src = e->h_bounce[s];
     }
-    CU(cudaMemcpyAsync(e->d_pages[s], src, m * PC_PAGE_SIZE, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(e->d_pages[s], src, m * PC_PAGE_SIZE, cudaMemcpyHostToDevice, sh));
     pc::PageDesc d{nullptr, nullptr, vaddr0 + 4096ull * p0, pid0};
     if (vaddrs) {
       std::memcpy(e->h_desc[s], vaddrs + p0, m * 8);
-      CU(cudaMemcpyAsync(e->d_vaddrs[s], e->h_desc[s], m * 8, cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(e->d_vaddrs[s], e->h_desc[s], m * 8, cudaMemcpyHostToDevice, sh));
       d.vaddrs = e->d_vaddrs[s];
     }
     if (pids) {
       std::memcpy(e->h_desc[s] + C * 8, pids + p0, m * 4);
-      CU(cudaMemcpyAsync(e->d_pids[s], e->h_desc[s] + C * 8, m * 4, cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(e->d_pids[s], e->h_desc[s] + C * 8, m * 4, cudaMemcpyHostToDevice, sh));
       d.pids = e->d_pids[s];
     }
-    int rc = launch_crypt(key, d, e->d_pages[s], e->d_pages[s], m, rounds, st);
+    if (dedicated) {
+      CU(cudaEventRecord(e->ev_h2d[s], sh));
+      CU(cudaStreamWaitEvent(sk, e->ev_h2d[s], 0));
+    }
+    int rc = launch_crypt(key, d, e->d_pages[s], e->d_pages[s], m, rounds, sk);
     if (rc != PC_OK) return rc;
+    if (dedicated) {
+      CU(cudaEventRecord(e->ev_k[s], sk));
+      CU(cudaStreamWaitEvent(sd, e->ev_k[s], 0));
+    }
     uint8_t *dst = pin_out ? dst_b + p0 * PC_PAGE_SIZE : e->h_bounce[s];
-    CU(cudaMemcpyAsync(dst, e->d_pages[s], m * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, st));
-    CU(cudaEventRecord(e->done[s], st));
+    CU(cudaMemcpyAsync(dst, e->d_pages[s], m * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, sd));
+    CU(cudaEventRecord(e->done[s], sd));
   }
-  const size_t first_pending =
-      (!pin_in || !pin_out || has_desc) && n_chunks > static_cast<size_t>(S) ? n_chunks - S : 0;
+  const size_t first_pending = n_chunks > static_cast<size_t>(S) ? n_chunks - S : 0;
   for (size_t c = first_pending; c < n_chunks; ++c) {
     int rc = finish(c);
     if (rc != PC_OK) return rc;
@@ -762,8 +847,13 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "kernel")) {
-    if (value != 1 && value != 2) return fail(PC_EINVAL, "kernel must be 1 or 2");
+    if (value < 1 || value > 3) return fail(PC_EINVAL, "kernel must be 1, 2 or 3");
     t.kernel = static_cast<int>(value);
+    return PC_OK;
+  }
+  if (!std::strcmp(knob, "host_mode")) {
+    if (value < 0 || value > 2) return fail(PC_EINVAL, "host_mode must be 0, 1 or 2");
+    t.host_mode = static_cast<int>(value);
     return PC_OK;
   }
   if (!std::strcmp(knob, "ctas_per_sm")) {
@@ -781,6 +871,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   else if (!std::strcmp(knob, "small_mode")) *value = t.small_mode;
   else if (!std::strcmp(knob, "small_max")) *value = static_cast<int64_t>(t.small_max.load());
   else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
+  else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;
   else if (!std::strcmp(knob, "ctas_per_sm")) *value = t.ctas_per_sm;
   else return fail(PC_EINVAL, "unknown knob '%s'", knob);
   return PC_OK;

@@ -127,7 +127,7 @@ class DeviceKey:
 class Engine:
     """Per-device streams + staging for host-resident batches."""
 
-    def __init__(self, device: int = 0, n_streams: int = 4, chunk_pages: int = 2048):
+    def __init__(self, device: int = 0, n_streams: int = 4, chunk_pages: int = 8192):
         h = ctypes.c_void_p()
         _native.call("pc_engine_create", device, n_streams, chunk_pages, ctypes.byref(h))
         self._handle = h.value
@@ -245,7 +245,7 @@ def _host_pids(pids, n: int):
         raise ContractViolation(f"pids must be integers, got {arr.dtype}")
     if arr.size and (int(arr.min()) < 0 or int(arr.max()) >= 2**32):
         raise ContractViolation("pid not a u32")
-    arr = np.ascontiguousarray(arr.astype(np.uint32)).reshape(-1)
+    arr = np.ascontiguousarray(arr.astype(np.uint32, copy=False)).reshape(-1)
     if arr.size != n:
         raise ContractViolation(f"{arr.size} pids for {n} pages")
     return arr, 0

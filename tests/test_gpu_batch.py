@@ -36,21 +36,41 @@ def t(x, device="cuda"):
     return torch.from_numpy(np.ascontiguousarray(x)).to(device)
 
 
+@pytest.fixture
+def knob():
+    """Set engine knobs for one test and restore them afterwards."""
+    from paper_2004_09252_b200 import _native
+
+    saved = {}
+
+    def set_(name, value):
+        saved.setdefault(name, _native.tune_get(name))
+        _native.tune(name, value)
+
+    yield set_
+    for name, value in saved.items():
+        _native.tune(name, value)
+
+
 class TestDevicePath:
+    @pytest.mark.parametrize("kernel", [1, 2, 3])
     @pytest.mark.parametrize("rounds", [8, 12, 20])
     @pytest.mark.parametrize("n", [1, 3, 64, 4097])
-    def test_contiguous_scalar_pid(self, dkey, n, rounds):
+    def test_contiguous_scalar_pid(self, dkey, n, rounds, kernel, knob):
         import torch
 
+        knob("kernel", kernel)
         pages = rand_pages(n, seed=n)
         got = pc.crypt_pages(dkey, BASE, 1, t(pages), rounds=rounds)
         torch.cuda.synchronize()
         want = C.crypt_pages(KEY, None, None, pages, rounds=rounds, vaddr0=BASE, pid0=1, nthreads=8)
         assert np.array_equal(got.cpu().numpy(), want)
 
-    def test_per_page_descriptors(self, dkey, ref_pages):
+    @pytest.mark.parametrize("kernel", [1, 2, 3])
+    def test_per_page_descriptors(self, dkey, ref_pages, kernel, knob):
         import torch
 
+        knob("kernel", kernel)
         r = ref_pages
         with pc.DeviceKey.install(r["key"].tobytes(), 0) as k:
             got = pc.crypt_pages(k, t(r["vaddrs"].view(np.int64)), t(r["pids"].view(np.int32)), t(r["pages"]))
@@ -65,9 +85,20 @@ class TestDevicePath:
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), r["ct"])
 
-    def test_pid_per_page_variant(self, dkey):
-        """pid = 1 + (i % 64)."""
+    @pytest.mark.parametrize("kernel", [1, 2, 3])
+    def test_pid_per_page_variant(self, dkey, kernel, knob):
+        """pid = 1 + (i % 64); also vaddr_hi changing mid-batch
+        (the v2/v3 kernels cache the vaddr_hi/pid column rounds)."""
         import torch
+
+        knob("kernel", kernel)
+        n = 3000
+        pages = rand_pages(n, 31)
+        v0 = 0x1_0000_0000 - 1500 * 4096  # crosses the 4 GiB boundary half way
+        got = pc.crypt_pages(dkey, v0, 9, t(pages))
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(),
+                              C.crypt_pages(KEY, None, None, pages, vaddr0=v0, pid0=9, nthreads=8))
 
         n = 2048
         pages = rand_pages(n, 3)
@@ -159,17 +190,21 @@ class TestHostPath:
         got = pc.crypt_pages(dkey, BASE, 3, pages)
         assert np.array_equal(got, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=3, nthreads=8))
 
-    @pytest.mark.parametrize("n", [1, 64, 9000])
-    def test_pinned_torch(self, dkey, n):
+    @pytest.mark.parametrize("host_mode", [0, 1, 2])
+    @pytest.mark.parametrize("n", [1, 64, 65, 9000])
+    def test_pinned_torch(self, dkey, n, host_mode, knob):
         import torch
 
+        knob("host_mode", host_mode)
         pages = rand_pages(n, 20 + n)
         src = torch.from_numpy(pages).pin_memory()
         dst = torch.empty_like(src).pin_memory()
         pc.crypt_pages(dkey, BASE, 4, src, out=dst)
         assert np.array_equal(dst.numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=4, nthreads=8))
 
-    def test_raw_key_host_with_descriptors(self, ref_pages):
+    @pytest.mark.parametrize("host_mode", [0, 1, 2])
+    def test_raw_key_host_with_descriptors(self, ref_pages, host_mode, knob):
+        knob("host_mode", host_mode)
         r = ref_pages
         got = pc.crypt_pages(r["key"].tobytes(), r["vaddrs"], r["pids"], r["pages"])
         assert np.array_equal(got, r["ct"])
@@ -184,6 +219,20 @@ class TestHostPath:
         buf = pages.copy()
         pc.crypt_pages(dkey, BASE, 5, buf, out=buf)
         assert np.array_equal(buf, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=5, nthreads=8))
+
+    @pytest.mark.parametrize("host_mode", [0, 1, 2])
+    def test_in_place_pinned_with_pinned_descriptors(self, dkey, host_mode, knob):
+        import torch
+
+        knob("host_mode", host_mode)
+        n = 1000
+        pages = rand_pages(n, 17)
+        buf = torch.from_numpy(pages.copy()).pin_memory()
+        va = torch.from_numpy((BASE + 4096 * np.arange(n, dtype=np.uint64)[::-1].copy()).view(np.int64)).pin_memory()
+        pi = torch.from_numpy((np.arange(n) % 7).astype(np.int32)).pin_memory()
+        pc.crypt_pages(dkey, va.numpy().view(np.uint64), pi.numpy().view(np.uint32), buf, out=buf)
+        want = C.crypt_pages(KEY, va.numpy().view(np.uint64), pi.numpy().view(np.uint32), pages, nthreads=8)
+        assert np.array_equal(buf.numpy(), want)
 
     def test_engine_stream_configs_agree(self, dkey):
         pages = rand_pages(5000, 8)

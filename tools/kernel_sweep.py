@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--rounds", default="8,12,20")
     ap.add_argument("--masks", default=",".join(hex(m) for m in MASKS))
-    ap.add_argument("--configs", default="k1:0,k2:0,k2:1,k2:2",
+    ap.add_argument("--configs", default="k1:0,k2:0,k3:0",
                     help="kernel:ctas_per_sm list (k1 sweeps --masks)")
     ap.add_argument("--no-intpeak", action="store_true")
     ap.add_argument("--trials", type=int, default=5)
@@ -51,7 +51,7 @@ def main():
         if kern == "k1":
             runs += [(1, 0, m) for m in [int(x, 0) for x in a.masks.split(",")]]
         else:
-            runs.append((2, int(ctas), 0))
+            runs.append((int(kern[1:]), int(ctas), 0))
     results = {}
     with pc.DeviceKey.install(key, 0) as dk:
         # ~1 s of untimed work first so SM clocks leave their idle state
