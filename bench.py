@@ -228,7 +228,7 @@ def main() -> None:
 
     import paper_2004_09252_b200 as pc
     from paper_2004_09252_b200 import _native
-    from paper_2004_09252_b200.partition import max_over_ranks
+    from paper_2004_09252_b200.partition import max_over_ranks, rank_pages
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -242,7 +242,7 @@ def main() -> None:
 
     n = args.pages
     # this rank's page range: disjoint vaddrs per rank (partition.shard of world*n)
-    vaddr0 = BASE_VADDR + PAGE * n * rank
+    _, _, vaddr0 = rank_pages(n, rank, world, BASE_VADDR)
     g = torch.Generator(device=dev).manual_seed(1 + rank)
     pages = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8, device=dev, generator=g)
     out = torch.empty_like(pages)
@@ -290,7 +290,7 @@ def main() -> None:
         return {
             "bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(rounds, n),
-            "kernel": "k_crypt_blocks", "launch_ms": round(k_ms, 4),
+            "kernel": "k_crypt_pages<%d>" % rounds, "launch_ms": round(k_ms, 4),
             "int32": {"achieved_tops": round(achieved * 1e9 * opb / 1e12, 3),
                       "peak_tops": round(peaks["arx_mix"] / 1e12, 3),
                       "ops_per_page": ops_per_page(rounds), "roof_gbs": round(int_roof, 1),

@@ -8,6 +8,7 @@
 #include <cstdint>
 
 #include "chacha.cuh"
+#include "tma.cuh"
 
 namespace pc {
 
@@ -245,6 +246,129 @@ k_crypt_pages_coalesced(const uint32_t *__restrict__ key, PageDesc desc, const u
     if (!has_next) break;
     page = next;
   }
+}
+
+// ---------------------------------------------------------------------------
+// v4: TMA pipeline.  The batch is viewed as a 2D tensor of 128-byte rows
+// (32 rows = one 4 KiB page per TMA box).  A CTA holds 4 independent page
+// slots of 64 threads (2 warps); slot k walks pages blockIdx.x*4 + k,
+// + 4*gridDim.x, ...  The slot's first thread keeps STAGES-1 pages in flight
+// with cp.async.bulk.tensor loads (SWIZZLE_128B, completion on the slot's
+// mbarrier), the slot's 64 threads compute their block's keystream (v2
+// hoisting) while the data lands, XOR it in shared memory (the 128B swizzle
+// makes the per-block LDS/STS.128 pattern bank-conflict-free), meet on a
+// 64-thread named barrier, and the leader writes the page back with a TMA
+// store.  No data registers are held across iterations, so bytes in flight
+// are set by shared memory (STAGES x 16 KiB per CTA), not by registers.
+constexpr int kPageRows = 32;
+constexpr int kPageBytes = 4096;
+
+__device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int ROUNDS, int STAGES>
+__global__ void __launch_bounds__(256, 3)
+k_crypt_pages_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                  const uint32_t *__restrict__ key, PageDesc desc, uint64_t n_pages) {
+  constexpr RotMul rm{};
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[4][STAGES];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t tid = threadIdx.x;
+  const uint32_t slot = tid >> 6;
+  const uint32_t b = tid & 63;
+  const bool leader = b == 0;
+  uint8_t *ring = smem + slot * (STAGES * kPageBytes);
+  uint64_t *bars = full[slot];
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 4;
+  const uint64_t page0 = static_cast<uint64_t>(blockIdx.x) * 4 + slot;
+  if (page0 >= n_pages) return; // whole slot (2 warps) leaves together
+  if (leader) {
+    if (slot == 0) {
+      prefetch_tmap(&tin);
+      prefetch_tmap(&tout);
+    }
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+#pragma unroll
+    for (int j = 0; j < STAGES - 1; ++j) {
+      const uint64_t pj = page0 + static_cast<uint64_t>(j) * stride;
+      if (pj < n_pages) {
+        mbar_arrive_expect_tx(&bars[j], kPageBytes);
+        tma_load_2d(ring + j * kPageBytes, &tin, 0, static_cast<int32_t>(pj * kPageRows), &bars[j]);
+      }
+    }
+  }
+  named_barrier_sync(1 + slot, 64); // barrier inits visible to the slot
+  uint32_t k[8];
+  load_key(key, k);
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
+  uint32_t cached_hi = 0, cached_pid = 0;
+  bool cached = false;
+  const uint32_t row = b >> 1;
+  const uint32_t chunk0 = (b & 1) * 4;
+  uint32_t off[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) off[c] = row * 128 + (((chunk0 + c) ^ (row & 7)) << 4);
+
+  for (uint32_t i = 0;; ++i) {
+    const uint64_t page = page0 + static_cast<uint64_t>(i) * stride;
+    if (page >= n_pages) break;
+    const uint32_t st = i % STAGES;
+    uint32_t s[4];
+    page_seed(desc, page, s);
+    if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+      cached_hi = s[1];
+      cached_pid = s[2];
+      cached = true;
+    }
+    uint32_t x[16];
+    x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
+    quarter_round<0>(x[0], x[4], x[8], x[12], rm);
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int r = 1; r < ROUNDS / 2; ++r) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    uint8_t *buf = ring + st * kPageBytes;
+    mbar_wait(&bars[st], (i / STAGES) & 1);
+    uint4 *p0 = reinterpret_cast<uint4 *>(buf + off[0]);
+    uint4 *p1 = reinterpret_cast<uint4 *>(buf + off[1]);
+    uint4 *p2 = reinterpret_cast<uint4 *>(buf + off[2]);
+    uint4 *p3 = reinterpret_cast<uint4 *>(buf + off[3]);
+    uint4 v0 = *p0, v1 = *p1, v2 = *p2, v3 = *p3;
+    v0.x ^= x[0] + kSigma0; v0.y ^= x[1] + kSigma1; v0.z ^= x[2] + kSigma2; v0.w ^= x[3] + kSigma3;
+    v1.x ^= x[4] + k[0]; v1.y ^= x[5] + k[1]; v1.z ^= x[6] + k[2]; v1.w ^= x[7] + k[3];
+    v2.x ^= x[8] + k[4]; v2.y ^= x[9] + k[5]; v2.z ^= x[10] + k[6]; v2.w ^= x[11] + k[7];
+    v3.x ^= x[12] + s[0]; v3.y ^= x[13] + s[1]; v3.z ^= x[14] + s[2]; v3.w ^= x[15] + b;
+    *p0 = v0; *p1 = v1; *p2 = v2; *p3 = v3;
+    fence_proxy_async_smem();
+    named_barrier_sync(1 + slot, 64);
+    if (leader) {
+      tma_store_2d(&tout, 0, static_cast<int32_t>(page * kPageRows), buf);
+      bulk_commit();
+      const uint64_t pn = page0 + static_cast<uint64_t>(i + STAGES - 1) * stride;
+      if (pn < n_pages) {
+        bulk_wait_read<1>(); // iteration i-1's store no longer reads the stage we refill
+        const uint32_t sn = (i + STAGES - 1) % STAGES;
+        mbar_arrive_expect_tx(&bars[sn], kPageBytes);
+        tma_load_2d(ring + sn * kPageBytes, &tin, 0, static_cast<int32_t>(pn * kPageRows), &bars[sn]);
+      }
+    }
+  }
+  if (leader) bulk_wait<0>();
 }
 
 // ---------------------------------------------------------------------------

@@ -7,6 +7,7 @@
 // (pkg/src/pagecrypt/workers.py: key slots :168,174-202,240-254; routing
 // :204-206 -> the page-range partitioner pc_crypt_pages_multi).
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -78,7 +79,8 @@ struct Tuning {
   std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
   std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
-  std::atomic<int> kernel{2};          // HBM kernel: 1 = k_crypt_blocks, 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced
+  std::atomic<int> kernel{2};          // HBM kernel: 1 = k_crypt_blocks, 2 = k_crypt_pages,
+                                       // 3 = k_crypt_pages_coalesced, 4 = k_crypt_pages_tma
   std::atomic<int> host_mode{2};       // large host batches: 0 = round-robin streams, 1 = zero-copy kernel
                                        // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams
   std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
@@ -161,12 +163,84 @@ void launch_pages_r(bool coalesced, const uint32_t *key, const pc::PageDesc &d, 
     pc::k_crypt_pages<R><<<pages_grid<R, false>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
 }
 
-// kernel_override: 0 = the "kernel" knob, else force 1/2/3 (the zero-copy
+// ---- v4: TMA pipeline --------------------------------------------------------
+constexpr int kTmaStages = 4;
+constexpr size_t kTmaSmem = 4 * kTmaStages * pc::kPageBytes + 1024; // 4 slots + 1 KiB alignment slack
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 2D view of n_pages pages: 128-byte rows, 32 per page; 128x128-byte boxes.
+int page_tensor_map(CUtensorMap *m, const void *base, uint64_t n_pages) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(PC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {128, n_pages * 32};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(pc::kPageRows)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return PC_OK;
+}
+
+template <int R>
+int launch_tma_r(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out, size_t n_pages,
+                 cudaStream_t st) {
+  static int sms[64] = {0}, occ[64] = {0};
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  dev &= 63;
+  auto kfn = pc::k_crypt_pages_tma<R, kTmaStages>;
+  if (!sms[dev]) {
+    CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem)));
+    CU(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    int o = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, 256, kTmaSmem));
+    occ[dev] = o > 0 ? o : 1;
+  }
+  // TMA row coordinates are int32: split batches above 2^25 pages
+  constexpr size_t kMaxPages = size_t(1) << 25;
+  for (size_t p0 = 0; p0 < n_pages; p0 += kMaxPages) {
+    const size_t m = std::min(kMaxPages, n_pages - p0);
+    CUtensorMap tin, tout;
+    int rc = page_tensor_map(&tin, static_cast<const uint8_t *>(in) + p0 * PC_PAGE_SIZE, m);
+    if (rc == PC_OK) rc = page_tensor_map(&tout, static_cast<uint8_t *>(out) + p0 * PC_PAGE_SIZE, m);
+    if (rc != PC_OK) return rc;
+    pc::PageDesc dd{d.vaddrs ? d.vaddrs + p0 : nullptr, d.pids ? d.pids + p0 : nullptr,
+                    d.vaddr0 + 4096ull * p0, d.pid0};
+    const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : occ[dev];
+    const uint64_t slots = (m + 3) / 4;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(static_cast<uint64_t>(sms[dev]) * per_sm, slots));
+    kfn<<<grid, 256, kTmaSmem, st>>>(tin, tout, key, dd, m);
+    CU(cudaGetLastError());
+  }
+  return PC_OK;
+}
+
+// kernel_override: 0 = the "kernel" knob, else force 1/2/3/4 (the zero-copy
 // host path forces 3).
 int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
                  size_t n_pages, int rounds, cudaStream_t st, int kernel_override = 0) {
   if (n_pages == 0) return PC_OK;
   const int kern = kernel_override ? kernel_override : tuning().kernel.load();
+  if (kern == 4) {
+    switch (rounds) {
+      case 8: return launch_tma_r<8>(key, d, in, out, n_pages, st);
+      case 12: return launch_tma_r<12>(key, d, in, out, n_pages, st);
+      default: return launch_tma_r<20>(key, d, in, out, n_pages, st);
+    }
+  }
   if (kern == 2 || kern == 3) {
     switch (rounds) {
       case 8: launch_pages_r<8>(kern == 3, key, d, in, out, n_pages, st); break;
@@ -847,7 +921,7 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "kernel")) {
-    if (value < 1 || value > 3) return fail(PC_EINVAL, "kernel must be 1, 2 or 3");
+    if (value < 1 || value > 4) return fail(PC_EINVAL, "kernel must be 1, 2, 3 or 4");
     t.kernel = static_cast<int>(value);
     return PC_OK;
   }

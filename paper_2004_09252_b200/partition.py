@@ -44,6 +44,18 @@ def shard(n: int, rank: int, world: int) -> tuple[int, int]:
     return page_ranges(n, world)[rank]
 
 
+def rank_pages(pages_per_rank: int, rank: int, world: int, base_vaddr: int) -> tuple[int, int, int]:
+    """Weak-scaling plan of the multi-GPU bench: the job is world *
+    pages_per_rank pages at contiguous vaddrs from base_vaddr, rank r owns
+    global pages [lo, hi) and therefore vaddrs from base_vaddr + 4096*lo.
+    Returns (lo, hi, vaddr0)."""
+    lo, hi = shard(pages_per_rank * world, rank, world)
+    vaddr0 = base_vaddr + PAGE_SIZE * lo
+    if vaddr0 % PAGE_SIZE or vaddr0 + PAGE_SIZE * max(hi - lo - 1, 0) >= 2**64:
+        raise ContractViolation("rank's vaddr range is not a valid u64 page range")
+    return lo, hi, vaddr0
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar over the default process group (the bench's
     timing reduction); identity when torch.distributed is not initialised."""
