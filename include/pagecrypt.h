@@ -38,6 +38,7 @@ extern "C" {
 #define PC_ECUDA 2  /* CUDA runtime/launch failure (message has the detail) */
 #define PC_ENOMEM 3 /* device or pinned allocation failed */
 #define PC_ESTATE 4 /* object used after destroy, wrong device, ... */
+#define PC_ETIMEOUT 5 /* a service request did not complete in time */
 
 #define PC_PAGE_SIZE 4096
 #define PC_BLOCK_SIZE 64
@@ -51,6 +52,7 @@ typedef struct pc_engine pc_engine; /* per-device streams + staging buffers */
 int pc_abi_version(void);          /* PC_ABI_VERSION below                 */
 const char *pc_last_error(void);   /* thread-local, never NULL             */
 int pc_device_count(int *count);
+int pc_device_info(int device, int *sm_count, int *cc_major, int *cc_minor);
 #define PC_ABI_VERSION 1
 
 /* ---- (i) kernel seam ---------------------------------------------------
@@ -114,6 +116,34 @@ int pc_crypt_pages_host(pc_engine *eng, const pc_key *key, const uint8_t *raw_ke
 int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, int n_dev,
                          const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
                          uint32_t pid0, const void *in, void *out, size_t n, int rounds);
+
+/* ---- (vii) persistent crypto-worker service -----------------------------
+ * The paper's GPU design and the B200 replacement of the
+ * reference's WorkerPool / WorkerRing / Completion
+ * (pkg/src/pagecrypt/workers.py:28-254): one persistent kernel whose
+ * n_workers 32-thread CTAs each serve a multiple-producer ring of ring_slots
+ * (power of two) requests in mapped pinned host memory.  The key is read
+ * into the workers' registers once; after pc_service_start returns the
+ * pc_key may be destroyed and the key then exists only in registers.
+ * submit copies one 4 KiB page into the worker's ring, registers `dst` (may
+ * equal src; may be NULL to discard) as the destination of the result and
+ * returns a ticket; it blocks while the ring is full (back-pressure, like
+ * WorkerRing.push), delivering finished results to free a slot.  The result
+ * reaches dst when any thread delivers it: wait/poll do, and so does a
+ * producer that needs the slot.  dst must stay valid until wait/poll report
+ * the ticket done.  stop refuses with PC_ESTATE while requests are in flight
+ * (WorkerPool.shutdown, workers.py:240-254). */
+typedef struct pc_service pc_service;
+int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int rounds, pc_service **out);
+int pc_service_submit(pc_service *svc, int worker, uint64_t vaddr, uint32_t pid, const void *src,
+                      void *dst, uint64_t *ticket);
+int pc_service_poll(pc_service *svc, int worker, uint64_t ticket, int *done);
+int pc_service_wait(pc_service *svc, int worker, uint64_t ticket, int64_t timeout_us);
+int pc_service_crypt(pc_service *svc, int worker, uint64_t vaddr, uint32_t pid, const void *src,
+                     void *dst, int64_t timeout_us);
+int pc_service_in_flight(pc_service *svc, uint64_t *n);
+int pc_service_max_workers(int device, int *n);
+int pc_service_stop(pc_service *svc);
 
 /* ---- pinned host memory helpers --------------------------------------- */
 int pc_host_alloc(size_t bytes, void **out);

@@ -22,7 +22,7 @@ from .errors import ContractViolation, NativeLibraryMissing, PageCryptError
 LIB_NAME = "libpagecrypt.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ESTATE = 0, 1, 2, 3, 4
+PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ESTATE, PC_ETIMEOUT = 0, 1, 2, 3, 4, 5
 
 c_void_p, c_size_t, c_int = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
 c_u32, c_u64 = ctypes.c_uint32, ctypes.c_uint64
@@ -33,6 +33,7 @@ SIGNATURES = {
     "pc_abi_version": (c_int, []),
     "pc_last_error": (ctypes.c_char_p, []),
     "pc_device_count": (c_int, [P(c_int)]),
+    "pc_device_info": (c_int, [c_int, P(c_int), P(c_int), P(c_int)]),
     "pc_keystream_words": (c_int, [c_void_p, c_u64, c_u32, c_void_p, c_size_t, c_void_p, c_int]),
     "pc_keystream_raw": (c_int, [c_void_p, c_void_p, c_size_t, c_int, c_void_p]),
     "pc_key_install": (c_int, [c_int, c_void_p, P(c_void_p)]),
@@ -47,6 +48,14 @@ SIGNATURES = {
                                     c_void_p, c_void_p, c_size_t, c_int]),
     "pc_crypt_pages_multi": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_u64, c_u32,
                                      c_void_p, c_void_p, c_size_t, c_int]),
+    "pc_service_start": (c_int, [c_void_p, c_int, c_int, c_int, P(c_void_p)]),
+    "pc_service_submit": (c_int, [c_void_p, c_int, c_u64, c_u32, c_void_p, c_void_p, P(c_u64)]),
+    "pc_service_poll": (c_int, [c_void_p, c_int, c_u64, P(c_int)]),
+    "pc_service_wait": (c_int, [c_void_p, c_int, c_u64, ctypes.c_int64]),
+    "pc_service_crypt": (c_int, [c_void_p, c_int, c_u64, c_u32, c_void_p, c_void_p, ctypes.c_int64]),
+    "pc_service_in_flight": (c_int, [c_void_p, P(c_u64)]),
+    "pc_service_max_workers": (c_int, [c_int, P(c_int)]),
+    "pc_service_stop": (c_int, [c_void_p]),
     "pc_host_alloc": (c_int, [c_size_t, P(c_void_p)]),
     "pc_host_free": (c_int, [c_void_p]),
     "pc_host_register": (c_int, [c_void_p, c_size_t]),
@@ -104,6 +113,12 @@ def tune_get(knob: str) -> int:
     v = ctypes.c_int64()
     call("pc_tune_get", knob.encode(), ctypes.byref(v))
     return v.value
+
+
+def device_info(device: int = 0) -> dict:
+    sms, ma, mi = c_int(), c_int(), c_int()
+    call("pc_device_info", device, ctypes.byref(sms), ctypes.byref(ma), ctypes.byref(mi))
+    return {"sm_count": sms.value, "cc": (ma.value, mi.value)}
 
 
 def device_count() -> int:

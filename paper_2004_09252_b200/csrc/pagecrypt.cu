@@ -10,7 +10,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
+#include <memory>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +24,7 @@
 
 #include "../../include/pagecrypt.h"
 #include "kernels.cuh"
+#include "service.cuh"
 
 namespace {
 
@@ -288,11 +291,16 @@ bool pinned_alias(const void *p, void **dev) {
   return true;
 }
 
-// Scratch for the synchronous keystream seams, one per device (guarded).
+// Per-device scratch for the synchronous seams and key staging (guarded): a
+// device buffer (stream-ordered allocation, so no call here ever forces a
+// device-wide synchronisation -- a persistent service kernel may be running)
+// and a pinned host buffer, so key material never passes through the
+// driver's own pageable-copy staging and is wiped right after each use.
 struct Scratch {
   std::mutex mu;
   void *d = nullptr;
   size_t cap = 0;
+  uint8_t *h = nullptr; // pinned, same capacity
   cudaStream_t st = nullptr;
 };
 Scratch &scratch(int dev) {
@@ -300,39 +308,52 @@ Scratch &scratch(int dev) {
   return s[dev & 63];
 }
 
+// Caller holds sc.mu and the device is current.
+int scratch_reserve(Scratch &sc, size_t need) {
+  if (!sc.st) CU(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+  if (sc.cap >= need) return PC_OK;
+  if (sc.d) {
+    CU(cudaFreeAsync(sc.d, sc.st));
+    CU(cudaStreamSynchronize(sc.st));
+  }
+  if (sc.h) {
+    wipe(sc.h, sc.cap);
+    CU(cudaFreeHost(sc.h));
+  }
+  sc.d = nullptr;
+  sc.h = nullptr;
+  sc.cap = 0;
+  const size_t cap = std::max<size_t>(need, 64 * 1024);
+  CU(cudaMallocAsync(&sc.d, cap, sc.st));
+  CU(cudaStreamSynchronize(sc.st));
+  CU(cudaHostAlloc(reinterpret_cast<void **>(&sc.h), cap, cudaHostAllocDefault));
+  sc.cap = cap;
+  return PC_OK;
+}
+
 int keystream_sync(const uint32_t kw[8], const uint32_t *seeds, size_t k, uint32_t *out, int rounds) {
   int dev = 0;
   CU(cudaGetDevice(&dev));
   Scratch &sc = scratch(dev);
   std::lock_guard<std::mutex> lk(sc.mu);
-  const size_t in_bytes = 32 + 16 * k;
-  const size_t need = 256 + 16 * k + 64 * k;
-  if (!sc.st) CU(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
-  if (sc.cap < need) {
-    if (sc.d) CU(cudaFree(sc.d));
-    sc.d = nullptr;
-    sc.cap = 0;
-    CU(cudaMalloc(&sc.d, need));
-    sc.cap = need;
-  }
-  std::vector<uint32_t> host(in_bytes / 4);
-  std::memcpy(host.data(), kw, 32);
-  std::memcpy(host.data() + 8, seeds, 16 * k);
+  const size_t out_off = 256 + 16 * k;
+  const size_t need = out_off + 64 * k;
+  int rc = scratch_reserve(sc, need);
+  if (rc != PC_OK) return rc;
+  // pinned staging: key at [0,32), seeds at [256, 256+16k), keystream after
+  std::memcpy(sc.h, kw, 32);
+  std::memcpy(sc.h + 256, seeds, 16 * k);
   uint8_t *d = static_cast<uint8_t *>(sc.d);
-  // key at d[0..32), seeds at d+256, out after the seeds
-  int rc = PC_OK;
-  cudaError_t e = cudaMemcpyAsync(d, host.data(), 32, cudaMemcpyHostToDevice, sc.st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d + 256, host.data() + 8, 16 * k, cudaMemcpyHostToDevice, sc.st);
+  cudaError_t e = cudaMemcpyAsync(d, sc.h, out_off, cudaMemcpyHostToDevice, sc.st);
   if (e == cudaSuccess) {
     rc = launch_keystream(reinterpret_cast<uint32_t *>(d), reinterpret_cast<uint32_t *>(d + 256), k,
-                          reinterpret_cast<uint32_t *>(d + 256 + 16 * k), rounds, sc.st);
-    if (rc == PC_OK)
-      e = cudaMemcpyAsync(out, d + 256 + 16 * k, 64 * k, cudaMemcpyDeviceToHost, sc.st);
+                          reinterpret_cast<uint32_t *>(d + out_off), rounds, sc.st);
+    if (rc == PC_OK) e = cudaMemcpyAsync(sc.h + out_off, d + out_off, 64 * k, cudaMemcpyDeviceToHost, sc.st);
   }
-  cudaError_t e2 = cudaMemsetAsync(d, 0, need, sc.st); // wipe key + keystream
+  cudaError_t e2 = cudaMemsetAsync(d, 0, need, sc.st); // wipe key + keystream on the device
   cudaError_t e3 = cudaStreamSynchronize(sc.st);
-  wipe(host.data(), 32);
+  if (rc == PC_OK && e == cudaSuccess && e3 == cudaSuccess) std::memcpy(out, sc.h + out_off, 64 * k);
+  wipe(sc.h, need);
   if (rc != PC_OK) return rc;
   if (e == cudaSuccess) e = e2;
   if (e == cudaSuccess) e = e3;
@@ -348,8 +369,75 @@ constexpr uint32_t kEngineMagic = 0x656e6731u; // "eng1"
 struct pc_key {
   uint32_t magic;
   int device;
-  uint32_t *d_words;
+  uint32_t *d_words;     // 256-byte device allocation, key in the first 32 bytes
+  cudaStream_t kst;      // key's private stream: depends on every device-path use
+  cudaEvent_t ev;
+  std::mutex mu;
 };
+
+namespace {
+// Make the key's private stream depend on the work just enqueued on `st`, so
+// pc_key_destroy can wait for every use without a device-wide synchronise.
+int note_key_use(pc_key *key, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(key->mu);
+  CU(cudaEventRecord(key->ev, st));
+  CU(cudaStreamWaitEvent(key->kst, key->ev, 0));
+  return PC_OK;
+}
+
+// Allocate a key object on `device` and fill its 32 bytes from `src` through
+// the pinned scratch (wiped afterwards).  If `derive`, src is entropy and the
+// key is derived on the device by k_keygen.
+int key_create(int device, const uint8_t *src, bool derive, pc_key **out) {
+  *out = nullptr;
+  DeviceGuard g(device);
+  CU(g.err);
+  auto *k = new pc_key();
+  k->magic = kKeyMagic;
+  k->device = device;
+  auto bail = [&](int rc) {
+    if (k->d_words) {
+      cudaMemsetAsync(k->d_words, 0, 256, k->kst);
+      cudaFreeAsync(k->d_words, k->kst);
+      cudaStreamSynchronize(k->kst);
+    }
+    if (k->ev) cudaEventDestroy(k->ev);
+    if (k->kst) cudaStreamDestroy(k->kst);
+    delete k;
+    return rc;
+  };
+#define CUK(call)                                                                       \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) return bail(fail(PC_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); \
+  } while (0)
+  CUK(cudaStreamCreateWithFlags(&k->kst, cudaStreamNonBlocking));
+  CUK(cudaEventCreateWithFlags(&k->ev, cudaEventDisableTiming));
+  CUK(cudaMallocAsync(reinterpret_cast<void **>(&k->d_words), 256, k->kst));
+  {
+    Scratch &sc = scratch(device);
+    std::lock_guard<std::mutex> lk(sc.mu);
+    int rc = scratch_reserve(sc, 256);
+    if (rc != PC_OK) return bail(rc);
+    std::memcpy(sc.h, src, 32);
+    // key (or entropy) lands at d_words[0..7] / d_words[8..15]
+    uint32_t *dst = derive ? k->d_words + 8 : k->d_words;
+    cudaError_t e = cudaMemcpyAsync(dst, sc.h, 32, cudaMemcpyHostToDevice, k->kst);
+    if (e == cudaSuccess && derive) {
+      pc::k_keygen<<<1, 1, 0, k->kst>>>(k->d_words + 8, k->d_words);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaMemsetAsync(k->d_words + 8, 0, 32, k->kst);
+    }
+    cudaError_t e2 = cudaStreamSynchronize(k->kst);
+    wipe(sc.h, 32);
+    if (e == cudaSuccess) e = e2;
+    CUK(e);
+  }
+#undef CUK
+  *out = k;
+  return PC_OK;
+}
+} // namespace
 
 struct pc_engine {
   uint32_t magic = kEngineMagic;
@@ -393,6 +481,14 @@ int pc_device_count(int *count) {
   return PC_OK;
 }
 
+int pc_device_info(int device, int *sm_count, int *cc_major, int *cc_minor) {
+  if (!sm_count || !cc_major || !cc_minor) return fail(PC_EINVAL, "NULL output");
+  CU(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device));
+  CU(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  CU(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  return PC_OK;
+}
+
 // ---- (i) kernel seam -------------------------------------------------------
 int pc_keystream_words(const uint32_t kw[8], uint64_t vaddr, uint32_t pid, const int64_t *idx,
                        size_t k, uint32_t *out, int rounds) {
@@ -431,43 +527,12 @@ int pc_keystream_raw(const uint8_t key[32], const uint8_t *seeds16, size_t k, in
 // ---- (iii) key residency ---------------------------------------------------
 int pc_key_install(int device, const uint8_t key[32], pc_key **out) {
   if (!key || !out) return fail(PC_EINVAL, "key/out is NULL");
-  *out = nullptr;
-  DeviceGuard g(device);
-  CU(g.err);
-  uint32_t *d = nullptr;
-  CU(cudaMalloc(&d, 256));
-  cudaError_t e = cudaMemcpy(d, key, 32, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    cudaFree(d);
-    CU(e);
-  }
-  *out = new pc_key{kKeyMagic, device, d};
-  return PC_OK;
+  return key_create(device, key, false, out);
 }
 
 int pc_key_generate(int device, const uint8_t entropy[32], pc_key **out) {
   if (!entropy || !out) return fail(PC_EINVAL, "entropy/out is NULL");
-  *out = nullptr;
-  DeviceGuard g(device);
-  CU(g.err);
-  uint32_t *d = nullptr;
-  CU(cudaMalloc(&d, 256));
-  // entropy at d[32..63] (scratch), key at d[0..31]
-  cudaError_t e = cudaMemcpy(d + 8, entropy, 32, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) {
-    pc::k_keygen<<<1, 1>>>(d + 8, d);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) e = cudaMemset(d + 8, 0, 32);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    cudaMemset(d, 0, 256);
-    cudaFree(d);
-    CU(e);
-  }
-  *out = new pc_key{kKeyMagic, device, d};
-  return PC_OK;
+  return key_create(device, entropy, true, out);
 }
 
 int pc_key_destroy(pc_key *key) {
@@ -475,13 +540,17 @@ int pc_key_destroy(pc_key *key) {
   if (key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
   DeviceGuard g(key->device);
   CU(g.err);
-  // wait for every stream that may still read the key, then zero and free it
-  CU(cudaDeviceSynchronize());
-  CU(cudaMemset(key->d_words, 0, 256));
-  CU(cudaDeviceSynchronize());
-  CU(cudaFree(key->d_words));
-  key->magic = 0;
-  key->d_words = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(key->mu);
+    // kst already waits for every device-path use of the key (note_key_use)
+    CU(cudaMemsetAsync(key->d_words, 0, 256, key->kst));
+    CU(cudaFreeAsync(key->d_words, key->kst));
+    CU(cudaStreamSynchronize(key->kst));
+    cudaEventDestroy(key->ev);
+    cudaStreamDestroy(key->kst);
+    key->magic = 0;
+    key->d_words = nullptr;
+  }
   delete key;
   return PC_OK;
 }
@@ -509,7 +578,10 @@ int pc_crypt_pages_dev(const pc_key *key, const uint64_t *vaddrs, const uint32_t
   DeviceGuard g(key->device);
   CU(g.err);
   const pc::PageDesc d{vaddrs, pids, vaddr0, pid0};
-  return launch_crypt(key->d_words, d, in, out, n, rounds, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = launch_crypt(key->d_words, d, in, out, n, rounds, st);
+  if (rc != PC_OK) return rc;
+  return note_key_use(const_cast<pc_key *>(key), st);
 }
 
 // ---- (v) host-resident batch ---------------------------------------------
@@ -550,18 +622,19 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
     CUE(cudaEventCreateWithFlags(&e->done[s], cudaEventDisableTiming));
     CUE(cudaEventCreateWithFlags(&e->ev_h2d[s], cudaEventDisableTiming));
     CUE(cudaEventCreateWithFlags(&e->ev_k[s], cudaEventDisableTiming));
-    CUE(cudaMalloc(&e->d_pages[s], chunk_pages * PC_PAGE_SIZE));
-    CUE(cudaMalloc(&e->d_vaddrs[s], chunk_pages * 8));
-    CUE(cudaMalloc(&e->d_pids[s], chunk_pages * 4));
+    CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_pages[s]), chunk_pages * PC_PAGE_SIZE, e->streams[0]));
+    CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_vaddrs[s]), chunk_pages * 8, e->streams[0]));
+    CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_pids[s]), chunk_pages * 4, e->streams[0]));
     CUE(cudaHostAlloc(&e->h_desc[s], chunk_pages * 12, cudaHostAllocDefault));
   }
   CUE(cudaHostAlloc(&e->h_key, 256, cudaHostAllocDefault));
-  CUE(cudaMalloc(&e->d_rawkey, 256));
+  CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_rawkey), 256, e->streams[0]));
   const size_t sm = tuning().small_max.load();
   e->small_bytes = 256 + sm * 16 + sm * PC_PAGE_SIZE;
   CUE(cudaHostAlloc(&e->h_small, e->small_bytes, cudaHostAllocMapped));
   CUE(cudaHostGetDevicePointer(reinterpret_cast<void **>(&e->hd_small), e->h_small, 0));
-  CUE(cudaMalloc(&e->d_small, e->small_bytes));
+  CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_small), e->small_bytes, e->streams[0]));
+  CUE(cudaStreamSynchronize(e->streams[0]));
 #undef CUE
   *out = e;
   return PC_OK;
@@ -573,14 +646,21 @@ int pc_engine_destroy(pc_engine *e) {
   DeviceGuard g(e->device);
   for (auto s : e->streams)
     if (s) cudaStreamSynchronize(s);
-  if (e->d_rawkey) { cudaMemset(e->d_rawkey, 0, 256); cudaDeviceSynchronize(); cudaFree(e->d_rawkey); }
+  // stream-ordered frees on stream 0: no device-wide synchronisation
+  cudaStream_t s0 = e->streams.empty() ? nullptr : e->streams[0];
+  if (s0) {
+    if (e->d_rawkey) { cudaMemsetAsync(e->d_rawkey, 0, 256, s0); cudaFreeAsync(e->d_rawkey, s0); }
+    if (e->d_small) { cudaMemsetAsync(e->d_small, 0, 256, s0); cudaFreeAsync(e->d_small, s0); }
+    for (size_t s = 0; s < e->streams.size(); ++s) {
+      if (e->d_pages[s]) cudaFreeAsync(e->d_pages[s], s0);
+      if (e->d_vaddrs[s]) cudaFreeAsync(e->d_vaddrs[s], s0);
+      if (e->d_pids[s]) cudaFreeAsync(e->d_pids[s], s0);
+    }
+    cudaStreamSynchronize(s0);
+  }
   if (e->h_key) { wipe(e->h_key, 256); cudaFreeHost(e->h_key); }
   if (e->h_small) { wipe(e->h_small, 256); cudaFreeHost(e->h_small); }
-  if (e->d_small) cudaFree(e->d_small);
   for (size_t s = 0; s < e->streams.size(); ++s) {
-    if (e->d_pages[s]) cudaFree(e->d_pages[s]);
-    if (e->d_vaddrs[s]) cudaFree(e->d_vaddrs[s]);
-    if (e->d_pids[s]) cudaFree(e->d_pids[s]);
     if (e->h_bounce[s]) cudaFreeHost(e->h_bounce[s]);
     if (e->h_desc[s]) cudaFreeHost(e->h_desc[s]);
     if (e->done[s]) cudaEventDestroy(e->done[s]);
@@ -831,6 +911,279 @@ int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, i
   return PC_OK;
 }
 
+} // extern "C"
+
+// ---- (vii) persistent crypto-worker service -------------------------------------
+namespace {
+constexpr uint32_t kServiceMagic = 0x73766331u; // "svc1"
+
+int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key, pc::SvcSlot *slots,
+                   uint4 *pages, uint32_t ring, const uint32_t *stop, uint32_t *started) {
+  switch (rounds) {
+    case 8: pc::k_service<8><<<workers, 32, 0, st>>>(key, slots, pages, ring, stop, started); break;
+    case 12: pc::k_service<12><<<workers, 32, 0, st>>>(key, slots, pages, ring, stop, started); break;
+    default: pc::k_service<20><<<workers, 32, 0, st>>>(key, slots, pages, ring, stop, started); break;
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+inline void cpu_relax() {
+#if defined(__x86_64__)
+  __builtin_ia32_pause();
+#endif
+}
+} // namespace
+
+struct pc_service {
+  uint32_t magic = kServiceMagic;
+  int device = 0;
+  int n_workers = 0;
+  uint32_t ring = 0;
+  int rounds = 20;
+  cudaStream_t st = nullptr;
+  pc::SvcSlot *h_slots = nullptr, *d_slots = nullptr; // mapped pinned
+  uint8_t *h_pages = nullptr, *d_pages = nullptr;     // mapped pinned
+  uint32_t *h_ctrl = nullptr, *d_ctrl = nullptr;      // [0] stop, [64..] started[w]
+  // Host-side slot protocol.  Slot j of a worker carries tickets j, j+R, ...
+  //   next[j]  = the ticket whose result is the next to be delivered in slot j
+  //   claim[j] = ticket a finisher may claim (CAS t -> t+R) to deliver it
+  //   dst[j]   = where the result of the slot's current ticket goes
+  // Any thread may deliver a finished result (a waiter, a poller, or a
+  // producer that needs the slot), so a full ring never deadlocks.
+  std::unique_ptr<std::atomic<uint64_t>[]> tail;  // per worker: next ticket
+  std::unique_ptr<std::atomic<uint64_t>[]> next;  // per slot
+  std::unique_ptr<std::atomic<uint64_t>[]> claim; // per slot
+  std::unique_ptr<std::atomic<void *>[]> dst;     // per slot
+  std::atomic<uint64_t> in_flight{0};
+  bool stopped = false;
+};
+
+extern "C" {
+
+int pc_service_max_workers(int device, int *n) {
+  if (!n) return fail(PC_EINVAL, "n is NULL");
+  DeviceGuard g(device);
+  CU(g.err);
+  int sms = 0, occ = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc::k_service<20>, 32, 0));
+  *n = sms * std::max(occ, 1);
+  return PC_OK;
+}
+
+int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int rounds, pc_service **out) {
+  if (!out) return fail(PC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  if (ring_slots < 1 || ring_slots > 4096 || (ring_slots & (ring_slots - 1)))
+    return fail(PC_EINVAL, "ring capacity %d not a power of two in 1..4096", ring_slots);
+  int maxw = 0;
+  int rc = pc_service_max_workers(key->device, &maxw);
+  if (rc != PC_OK) return rc;
+  if (n_workers < 1 || n_workers > maxw)
+    return fail(PC_EINVAL, "n_workers must be 1..%d (all workers must be co-resident), got %d", maxw, n_workers);
+  DeviceGuard g(key->device);
+  CU(g.err);
+  auto *s = new pc_service();
+  s->device = key->device;
+  s->n_workers = n_workers;
+  s->ring = static_cast<uint32_t>(ring_slots);
+  s->rounds = rounds;
+  const size_t nslots = static_cast<size_t>(n_workers) * ring_slots;
+  s->tail.reset(new std::atomic<uint64_t>[n_workers]);
+  s->next.reset(new std::atomic<uint64_t>[nslots]);
+  s->claim.reset(new std::atomic<uint64_t>[nslots]);
+  s->dst.reset(new std::atomic<void *>[nslots]);
+  for (int w = 0; w < n_workers; ++w) s->tail[w] = 0;
+  for (size_t i = 0; i < nslots; ++i) {
+    s->next[i] = i % ring_slots;
+    s->claim[i] = i % ring_slots;
+    s->dst[i] = nullptr;
+  }
+  auto bail = [&](int code) {
+    if (s->h_slots) cudaFreeHost(s->h_slots);
+    if (s->h_pages) cudaFreeHost(s->h_pages);
+    if (s->h_ctrl) cudaFreeHost(s->h_ctrl);
+    if (s->st) cudaStreamDestroy(s->st);
+    delete s;
+    return code;
+  };
+#define CUS(call)                                                                       \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) return bail(fail(PC_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); \
+  } while (0)
+  CUS(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_slots), nslots * sizeof(pc::SvcSlot), cudaHostAllocMapped));
+  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_pages), nslots * PC_PAGE_SIZE, cudaHostAllocMapped));
+  const size_t ctrl_bytes = (64 + static_cast<size_t>(n_workers)) * 4;
+  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_ctrl), ctrl_bytes, cudaHostAllocMapped));
+  std::memset(s->h_slots, 0, nslots * sizeof(pc::SvcSlot));
+  std::memset(s->h_pages, 0, nslots * PC_PAGE_SIZE);
+  std::memset(s->h_ctrl, 0, ctrl_bytes);
+  CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_slots), s->h_slots, 0));
+  CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_pages), s->h_pages, 0));
+  CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_ctrl), s->h_ctrl, 0));
+#undef CUS
+  // the kernel reads the key once; it must be resident before we report success
+  rc = service_launch(rounds, n_workers, s->st, key->d_words, s->d_slots, reinterpret_cast<uint4 *>(s->d_pages),
+                      s->ring, s->d_ctrl, s->d_ctrl + 64);
+  if (rc != PC_OK) return bail(rc);
+  const auto t0 = std::chrono::steady_clock::now();
+  volatile uint32_t *started = s->h_ctrl + 64;
+  for (int w = 0; w < n_workers; ++w) {
+    while (started[w] == 0) {
+      if (cudaStreamQuery(s->st) != cudaErrorNotReady) {
+        cudaError_t e = cudaStreamSynchronize(s->st);
+        return bail(fail(PC_ECUDA, "service kernel exited during start: %s", cudaGetErrorString(e)));
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+        s->h_ctrl[0] = 1; // ask the resident workers to leave
+        cudaStreamSynchronize(s->st);
+        return bail(fail(PC_ETIMEOUT, "service workers did not start (%d of %d)", w, n_workers));
+      }
+      std::this_thread::yield();
+    }
+  }
+  *out = s;
+  return PC_OK;
+}
+
+} // extern "C"
+
+namespace {
+inline size_t svc_slot(const pc_service *s, int worker, uint64_t t) {
+  return static_cast<size_t>(worker) * s->ring + (t % s->ring);
+}
+
+// Deliver ticket t's result if the GPU has finished it and nobody else is
+// delivering it.  Returns true when t is delivered (by us or someone else).
+bool svc_try_finish(pc_service *s, int worker, uint64_t t) {
+  const size_t slot = svc_slot(s, worker, t);
+  if (s->next[slot].load(std::memory_order_acquire) > t) return true;
+  const uint64_t d = *reinterpret_cast<volatile uint64_t *>(&s->h_slots[slot].done_seq);
+  if (d != t + 1) return false;
+  uint64_t expect = t;
+  if (!s->claim[slot].compare_exchange_strong(expect, t + s->ring, std::memory_order_acq_rel))
+    return false; // another thread is delivering it
+  std::atomic_thread_fence(std::memory_order_acquire);
+  uint8_t *page = s->h_pages + slot * PC_PAGE_SIZE;
+  void *dst = s->dst[slot].load(std::memory_order_acquire);
+  if (dst) std::memcpy(dst, page, PC_PAGE_SIZE);
+  wipe(page, PC_PAGE_SIZE); // the ring page held a plaintext or ciphertext copy
+  s->dst[slot].store(nullptr, std::memory_order_relaxed);
+  s->in_flight.fetch_sub(1, std::memory_order_relaxed);
+  s->next[slot].store(t + s->ring, std::memory_order_release);
+  return true;
+}
+
+int svc_check(pc_service *s, int worker) {
+  if (!s || s->magic != kServiceMagic) return fail(PC_ESTATE, "not a live pc_service");
+  if (worker < 0 || worker >= s->n_workers) return fail(PC_EINVAL, "worker %d out of range", worker);
+  return PC_OK;
+}
+} // namespace
+
+extern "C" {
+
+int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
+                      uint64_t *ticket) {
+  int rc = svc_check(s, worker);
+  if (rc != PC_OK) return rc;
+  if (s->stopped) return fail(PC_ESTATE, "service is not running");
+  if (!src || !ticket) return fail(PC_EINVAL, "src/ticket is NULL");
+  const uint64_t t = s->tail[worker].fetch_add(1, std::memory_order_relaxed);
+  const size_t slot = svc_slot(s, worker, t);
+  // back-pressure (WorkerRing.push blocks while full): the slot's previous
+  // ticket must be delivered; help deliver it if the GPU is done with it
+  uint32_t spins = 0;
+  while (s->next[slot].load(std::memory_order_acquire) != t) {
+    if (t >= s->ring) svc_try_finish(s, worker, t - s->ring);
+    if (++spins > 64) std::this_thread::yield();
+    else cpu_relax();
+  }
+  s->in_flight.fetch_add(1, std::memory_order_relaxed);
+  pc::SvcSlot *sl = s->h_slots + slot;
+  std::memcpy(s->h_pages + slot * PC_PAGE_SIZE, src, PC_PAGE_SIZE);
+  s->dst[slot].store(dst, std::memory_order_relaxed);
+  sl->vaddr = vaddr;
+  sl->pid = pid;
+  std::atomic_thread_fence(std::memory_order_release);
+  *reinterpret_cast<volatile uint64_t *>(&sl->ready_seq) = t + 1;
+  *ticket = t;
+  return PC_OK;
+}
+
+int pc_service_poll(pc_service *s, int worker, uint64_t t, int *done) {
+  int rc = svc_check(s, worker);
+  if (rc != PC_OK) return rc;
+  if (!done) return fail(PC_EINVAL, "done is NULL");
+  if (t >= s->tail[worker].load(std::memory_order_relaxed)) return fail(PC_EINVAL, "ticket %llu not issued", (unsigned long long)t);
+  *done = svc_try_finish(s, worker, t) ? 1 : 0;
+  return PC_OK;
+}
+
+int pc_service_wait(pc_service *s, int worker, uint64_t t, int64_t timeout_us) {
+  int rc = svc_check(s, worker);
+  if (rc != PC_OK) return rc;
+  if (t >= s->tail[worker].load(std::memory_order_relaxed)) return fail(PC_EINVAL, "ticket %llu not issued", (unsigned long long)t);
+  const auto t0 = std::chrono::steady_clock::now();
+  uint32_t spins = 0;
+  while (!svc_try_finish(s, worker, t)) {
+    if (++spins < 4096) {
+      cpu_relax();
+      continue;
+    }
+    spins = 0;
+    if (timeout_us >= 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(timeout_us))
+      return fail(PC_ETIMEOUT, "timed out waiting for crypto completion");
+    if (cudaStreamQuery(s->st) != cudaErrorNotReady) return fail(PC_ECUDA, "service kernel is no longer running");
+    std::this_thread::yield();
+  }
+  return PC_OK;
+}
+
+int pc_service_crypt(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
+                     int64_t timeout_us) {
+  uint64_t t = 0;
+  int rc = pc_service_submit(s, worker, vaddr, pid, src, dst, &t);
+  if (rc != PC_OK) return rc;
+  return pc_service_wait(s, worker, t, timeout_us);
+}
+
+int pc_service_in_flight(pc_service *s, uint64_t *n) {
+  if (!s || s->magic != kServiceMagic) return fail(PC_ESTATE, "not a live pc_service");
+  if (!n) return fail(PC_EINVAL, "n is NULL");
+  *n = s->in_flight.load();
+  return PC_OK;
+}
+
+int pc_service_stop(pc_service *s) {
+  if (!s || s->magic != kServiceMagic) return fail(PC_ESTATE, "not a live pc_service");
+  const uint64_t n = s->in_flight.load();
+  if (n) return fail(PC_ESTATE, "%llu requests in flight", (unsigned long long)n);
+  DeviceGuard g(s->device);
+  CU(g.err);
+  s->stopped = true;
+  *reinterpret_cast<volatile uint32_t *>(s->h_ctrl) = 1;
+  cudaError_t e = cudaStreamSynchronize(s->st);
+  const size_t nslots = static_cast<size_t>(s->n_workers) * s->ring;
+  wipe(s->h_pages, nslots * PC_PAGE_SIZE);
+  cudaFreeHost(s->h_slots);
+  cudaFreeHost(s->h_pages);
+  cudaFreeHost(s->h_ctrl);
+  cudaStreamDestroy(s->st);
+  s->magic = 0;
+  delete s;
+  CU(e);
+  return PC_OK;
+}
+
+} // extern "C"
+
+extern "C" {
 // ---- pinned memory ---------------------------------------------------------
 int pc_host_alloc(size_t bytes, void **out) {
   if (!out) return fail(PC_EINVAL, "out is NULL");
@@ -862,20 +1215,22 @@ int pc_intpeak(int device, int kind, double *ops_per_s) {
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   uint32_t *sink = nullptr;
-  CU(cudaMalloc(&sink, 1024 * 4));
+  cudaStream_t st = nullptr;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CU(cudaMallocAsync(reinterpret_cast<void **>(&sink), 1024 * 4, st));
   const dim3 grid(sms * 8), block(256);
   const bool arx = kind == 4 || kind == 5;
   const int iters = arx ? 1000 : 1500;
   auto run = [&](int it) {
     switch (kind) {
-      case 0: pc::k_intpeak<0><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      case 1: pc::k_intpeak<1><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      case 2: pc::k_intpeak<2><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      case 3: pc::k_intpeak<3><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      case 4: pc::k_intpeak<4><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      case 5: pc::k_intpeak<5><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      case 6: pc::k_intpeak<6><<<grid, block>>>(1u, kRotMul, it, sink); break;
-      default: pc::k_intpeak<7><<<grid, block>>>(1u, kRotMul, it, sink); break;
+      case 0: pc::k_intpeak<0><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      case 1: pc::k_intpeak<1><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      case 2: pc::k_intpeak<2><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      case 3: pc::k_intpeak<3><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      case 4: pc::k_intpeak<4><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      case 5: pc::k_intpeak<5><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      case 6: pc::k_intpeak<6><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
+      default: pc::k_intpeak<7><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
     }
   };
   cudaEvent_t a, b;
@@ -884,9 +1239,9 @@ int pc_intpeak(int device, int kind, double *ops_per_s) {
   run(iters / 10); // warm-up
   float best_ms = 1e30f;
   for (int rep = 0; rep < 5; ++rep) {
-    CU(cudaEventRecord(a));
+    CU(cudaEventRecord(a, st));
     run(iters);
-    CU(cudaEventRecord(b));
+    CU(cudaEventRecord(b, st));
     CU(cudaEventSynchronize(b));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, a, b));
@@ -895,7 +1250,9 @@ int pc_intpeak(int device, int kind, double *ops_per_s) {
   CU(cudaGetLastError());
   cudaEventDestroy(a);
   cudaEventDestroy(b);
-  cudaFree(sink);
+  cudaFreeAsync(sink, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
   // ops per iteration: ARX = 16 quarter rounds x 12 ops (op-count convention,
   // independent of how many instructions implement them); others 16 x 8 chains
   // (kind 7 counts IMAD.WIDE + its LOP3 as 2 ops).

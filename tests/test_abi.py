@@ -72,3 +72,18 @@ def test_no_cpu_fallback_without_gpu():
         pc.page_keystream(bytes(32), 0, 0)
     with pytest.raises(PageCryptError):
         pc.DeviceKey.install(bytes(32), 0)
+
+
+def test_no_kernel_uses_local_memory():
+    """Key and cipher state stay in registers in every kernel (PAPER.md:634-637:
+    "the current implementation of the GPU kernel never does register
+    spilling")."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", _native.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    fns = re.findall(r"Function (\S+):\n\s+REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
+    assert len(fns) >= 20
+    names = " ".join(f[0] for f in fns)
+    for k in ("k_crypt_pages", "k_crypt_pages_tma", "k_service", "k_keystream_seeds", "k_keygen"):
+        assert k in names
+    bad = [(f, st, lo) for f, _, st, lo in fns if st != "0" or lo != "0"]
+    assert not bad
