@@ -142,6 +142,9 @@ int pc_service_wait(pc_service *svc, int worker, uint64_t ticket, int64_t timeou
 int pc_service_crypt(pc_service *svc, int worker, uint64_t vaddr, uint32_t pid, const void *src,
                      void *dst, int64_t timeout_us);
 int pc_service_in_flight(pc_service *svc, uint64_t *n);
+/* Diagnostics: device %globaltimer stamps of the slot's last request (bell
+ * seen, page loaded, keystream done, page written back). */
+int pc_service_timing(pc_service *svc, int worker, uint64_t ticket, uint64_t out_ns[4]);
 int pc_service_max_workers(int device, int *n);
 int pc_service_stop(pc_service *svc);
 

@@ -54,6 +54,7 @@ SIGNATURES = {
     "pc_service_wait": (c_int, [c_void_p, c_int, c_u64, ctypes.c_int64]),
     "pc_service_crypt": (c_int, [c_void_p, c_int, c_u64, c_u32, c_void_p, c_void_p, ctypes.c_int64]),
     "pc_service_in_flight": (c_int, [c_void_p, P(c_u64)]),
+    "pc_service_timing": (c_int, [c_void_p, c_int, c_u64, P(c_u64)]),
     "pc_service_max_workers": (c_int, [c_int, P(c_int)]),
     "pc_service_stop": (c_int, [c_void_p]),
     "pc_host_alloc": (c_int, [c_size_t, P(c_void_p)]),

@@ -918,11 +918,14 @@ namespace {
 constexpr uint32_t kServiceMagic = 0x73766331u; // "svc1"
 
 int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key, pc::SvcSlot *slots,
-                   uint4 *pages, uint32_t ring, const uint32_t *stop, uint32_t *started) {
+                   uint4 *pages, uint32_t ring, const uint64_t *bell, const uint32_t *stop, uint32_t *started,
+                   pc::SvcDev *dev) {
+  const unsigned grid = static_cast<unsigned>(workers) + 1; // + the dispatcher
+  const uint32_t nw = static_cast<uint32_t>(workers);
   switch (rounds) {
-    case 8: pc::k_service<8><<<workers, 32, 0, st>>>(key, slots, pages, ring, stop, started); break;
-    case 12: pc::k_service<12><<<workers, 32, 0, st>>>(key, slots, pages, ring, stop, started); break;
-    default: pc::k_service<20><<<workers, 32, 0, st>>>(key, slots, pages, ring, stop, started); break;
+    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev); break;
+    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev); break;
+    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev); break;
   }
   CU(cudaGetLastError());
   return PC_OK;
@@ -945,6 +948,8 @@ struct pc_service {
   pc::SvcSlot *h_slots = nullptr, *d_slots = nullptr; // mapped pinned
   uint8_t *h_pages = nullptr, *d_pages = nullptr;     // mapped pinned
   uint32_t *h_ctrl = nullptr, *d_ctrl = nullptr;      // [0] stop, [64..] started[w]
+  uint64_t *h_bell = nullptr, *d_bell = nullptr;      // per worker: tickets published (in order)
+  pc::SvcDev *dev = nullptr;                          // device-memory doorbell mirror
   // Host-side slot protocol.  Slot j of a worker carries tickets j, j+R, ...
   //   next[j]  = the ticket whose result is the next to be delivered in slot j
   //   claim[j] = ticket a finisher may claim (CAS t -> t+R) to deliver it
@@ -967,8 +972,8 @@ int pc_service_max_workers(int device, int *n) {
   CU(g.err);
   int sms = 0, occ = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc::k_service<20>, 32, 0));
-  *n = sms * std::max(occ, 1);
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc::k_service<20>, 64, 0));
+  *n = std::min(sms * std::max(occ, 1) - 1, 4096); // one CTA is the dispatcher
   return PC_OK;
 }
 
@@ -1003,9 +1008,14 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     s->dst[i] = nullptr;
   }
   auto bail = [&](int code) {
+    if (s->dev) {
+      cudaFreeAsync(s->dev, s->st);
+      cudaStreamSynchronize(s->st);
+    }
     if (s->h_slots) cudaFreeHost(s->h_slots);
     if (s->h_pages) cudaFreeHost(s->h_pages);
     if (s->h_ctrl) cudaFreeHost(s->h_ctrl);
+    if (s->h_bell) cudaFreeHost(s->h_bell);
     if (s->st) cudaStreamDestroy(s->st);
     delete s;
     return code;
@@ -1026,10 +1036,16 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_slots), s->h_slots, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_pages), s->h_pages, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_ctrl), s->h_ctrl, 0));
+  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(uint64_t), cudaHostAllocMapped));
+  std::memset(s->h_bell, 0, n_workers * sizeof(uint64_t));
+  CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_bell), s->h_bell, 0));
+  CUS(cudaMallocAsync(reinterpret_cast<void **>(&s->dev), sizeof(pc::SvcDev), s->st));
+  CUS(cudaMemsetAsync(s->dev, 0, sizeof(pc::SvcDev), s->st));
+  CUS(cudaStreamSynchronize(s->st));
 #undef CUS
   // the kernel reads the key once; it must be resident before we report success
   rc = service_launch(rounds, n_workers, s->st, key->d_words, s->d_slots, reinterpret_cast<uint4 *>(s->d_pages),
-                      s->ring, s->d_ctrl, s->d_ctrl + 64);
+                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev);
   if (rc != PC_OK) return bail(rc);
   const auto t0 = std::chrono::steady_clock::now();
   volatile uint32_t *started = s->h_ctrl + 64;
@@ -1111,7 +1127,14 @@ int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, c
   sl->vaddr = vaddr;
   sl->pid = pid;
   std::atomic_thread_fence(std::memory_order_release);
-  *reinterpret_cast<volatile uint64_t *>(&sl->ready_seq) = t + 1;
+  // publish in ticket order: the doorbell counts consecutive published tickets
+  auto *bell = reinterpret_cast<std::atomic<uint64_t> *>(s->h_bell + worker);
+  uint32_t bspins = 0;
+  while (bell->load(std::memory_order_acquire) != t) {
+    if (++bspins > 64) std::this_thread::yield();
+    else cpu_relax();
+  }
+  bell->store(t + 1, std::memory_order_release);
   *ticket = t;
   return PC_OK;
 }
@@ -1153,6 +1176,15 @@ int pc_service_crypt(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, co
   return pc_service_wait(s, worker, t, timeout_us);
 }
 
+int pc_service_timing(pc_service *s, int worker, uint64_t t, uint64_t out_ns[4]) {
+  int rc = svc_check(s, worker);
+  if (rc != PC_OK) return rc;
+  if (!out_ns) return fail(PC_EINVAL, "out is NULL");
+  const pc::SvcSlot *sl = s->h_slots + svc_slot(s, worker, t);
+  for (int i = 0; i < 4; ++i) out_ns[i] = reinterpret_cast<const volatile uint64_t *>(sl->t_ns)[i];
+  return PC_OK;
+}
+
 int pc_service_in_flight(pc_service *s, uint64_t *n) {
   if (!s || s->magic != kServiceMagic) return fail(PC_ESTATE, "not a live pc_service");
   if (!n) return fail(PC_EINVAL, "n is NULL");
@@ -1171,9 +1203,12 @@ int pc_service_stop(pc_service *s) {
   cudaError_t e = cudaStreamSynchronize(s->st);
   const size_t nslots = static_cast<size_t>(s->n_workers) * s->ring;
   wipe(s->h_pages, nslots * PC_PAGE_SIZE);
+  cudaFreeAsync(s->dev, s->st);
+  cudaStreamSynchronize(s->st);
   cudaFreeHost(s->h_slots);
   cudaFreeHost(s->h_pages);
   cudaFreeHost(s->h_ctrl);
+  cudaFreeHost(s->h_bell);
   cudaStreamDestroy(s->st);
   s->magic = 0;
   delete s;

@@ -231,7 +231,13 @@ def _scan_process_memory(key_ints: list[int], length: int = 16) -> int:
         for parts in regions:
             lo, hi = (int(x, 16) for x in parts[0].split("-"))
             path = parts[5] if len(parts) > 5 else ""
-            if "r" not in parts[1] or path.startswith("/dev/") or path.startswith("[v"):
+            # private writable memory: heap, stacks, anonymous maps (Python
+            # objects, malloc, the library's staging) and writable data of
+            # loaded objects; device-file mappings (/dev/nvidia*) are skipped:
+            # reading them through /proc/self/mem is not supported
+            if not parts[1].startswith("rw") or path.startswith("/dev/") or path.startswith("[v"):
+                continue
+            if hi - lo > (4 << 30):
                 continue
             pos = lo
             while pos < hi:
