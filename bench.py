@@ -28,7 +28,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -54,60 +53,61 @@ def ops_per_page(rounds: int) -> int:
 
 
 class ClockSampler:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event reasons sampled every few ms by NVML
+    (nvidia-smi's source) in a background thread during the timed region --
+    fast enough for regions of a few tens of ms.  Falls back to nvidia-smi."""
 
-    def __init__(self, gpu_index: int):
+    REASONS = {  # NVML clock-event bits we report
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4,
+    }
+
+    def __init__(self, gpu_index: int, period_s: float = 0.002):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.samples: list[tuple[float, float, float, int]] = []
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
-            time.sleep(0.25)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+        except Exception:
+            self._nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((time.perf_counter(), float(sm), pw, int(rs)))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.15)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._nvml is not None:
+            self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, pw, reasons = [], [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1])); mx.append(float(f[2])); pw.append(float(f[3]))
-            except ValueError:
-                continue
-            for name, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "power_w_max": max(pw), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "unavailable"}
+        sm = [x[1] for x in self.samples]
+        reasons = sorted({name for _, _, _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "power_w_max": round(max(x[2] for x in self.samples), 1),
+                "samples": len(sm), "source": "NVML every %g ms during the timed region" % (1e3 * self.period)}
 
 
 # ---------------------------------------------------------------------------
@@ -334,6 +334,7 @@ def main() -> None:
                                     "unit": "GB/s", "roofline": roofline(r, ms)}
         if rank == 0:
             extras["latency_host_small"] = latency_sweep(pc, key, local_rank)
+            extras["latency_service_1page"] = service_latency(local_rank)
     del host_in, host_out
 
     cpu = None
@@ -400,6 +401,46 @@ def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
         p50 = ts[len(ts) // 2] / 1e3
         res[str(n)] = {"p50_us": round(p50, 2), "p99_us": round(ts[int(len(ts) * 0.99)] / 1e3, 2),
                        "gbps_at_p50": round(n * PAGE / (p50 * 1e-6) / 1e9, 3)}
+    return res
+
+
+def service_latency(device: int, reps: int = 2000) -> dict:
+    """BASELINE configs[3] through the persistent GPU worker service (the
+    paper's design; WorkerPool drop-in): 1-page fault-path requests."""
+    import ctypes
+
+    from paper_2004_09252_b200 import _native
+    from paper_2004_09252_b200.workers import ClientId, WorkerPool
+
+    res = {}
+    pool = WorkerPool(keysource=os.urandom, device=device)
+    try:
+        page = bytearray(PAGE)
+        c = ClientId(1, 0)
+        for _ in range(100):
+            pool.crypt(c, BASE_VADDR, "encrypt", page)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter_ns()
+            pool.crypt(c, BASE_VADDR, "encrypt", page)
+            ts.append(time.perf_counter_ns() - t0)
+        ts.sort()
+        res["WorkerPool.crypt"] = {"p50_us": round(ts[len(ts) // 2] / 1e3, 2),
+                                   "p99_us": round(ts[int(len(ts) * .99)] / 1e3, 2)}
+        lib = _native.load()
+        buf = (ctypes.c_char * PAGE)()
+        w = pool.route(c)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter_ns()
+            lib.pc_service_crypt(pool._svc, w, BASE_VADDR, 1, buf, buf, -1)
+            ts.append(time.perf_counter_ns() - t0)
+        ts.sort()
+        res["pc_service_crypt"] = {"p50_us": round(ts[len(ts) // 2] / 1e3, 2),
+                                   "p99_us": round(ts[int(len(ts) * .99)] / 1e3, 2)}
+        res["workers"] = pool.n_workers
+    finally:
+        pool.shutdown()
     return res
 
 
