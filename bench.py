@@ -290,7 +290,8 @@ def main() -> None:
         return {
             "bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(rounds, n),
-            "kernel": "k_crypt_pages<%d>" % rounds, "launch_ms": round(k_ms, 4),
+            "kernel": ("k_crypt_pages_coalesced<8>" if rounds == 8 else "k_crypt_pages_async<%d>" % rounds),
+            "launch_ms": round(k_ms, 4),
             "int32": {"achieved_tops": round(achieved * 1e9 * opb / 1e12, 3),
                       "peak_tops": round(peaks["arx_mix"] / 1e12, 3),
                       "ops_per_page": ops_per_page(rounds), "roof_gbs": round(int_roof, 1),

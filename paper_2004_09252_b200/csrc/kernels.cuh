@@ -372,6 +372,103 @@ k_crypt_pages_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant
 }
 
 // ---------------------------------------------------------------------------
+// v5: the v2 page loop with a cp.async (LDGSTS) ring instead of register
+// prefetch.  Each thread streams its own 64-byte block of the pages 1 and 2
+// strides ahead into a 3-stage shared-memory ring (no registers held, so
+// occupancy is 4 CTAs/SM and ~128 KiB per SM is in flight), waits for the
+// current page's group, XORs and stores.  The 4 chunks of a thread's block
+// sit at XOR-swizzled positions c ^ ((t >> 1) & 3), which makes the per-thread
+// 64-byte LDS/STS pattern bank-conflict-free while each chunk keeps a static
+// register.  Only the issuing thread reads its own copies, so no barrier is
+// needed (cp.async.wait_group gives the thread visibility).
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void *gptr) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int ROUNDS>
+__global__ void __launch_bounds__(256, 4)
+k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
+                    uint64_t n_pages) {
+  constexpr RotMul rm{};
+  constexpr int kStages = 3;
+  __shared__ uint4 ring[kStages][256 * 4]; // 16 KiB per stage
+  const uint32_t tid = threadIdx.x;
+  const uint32_t b = tid & 63;
+  const uint32_t sw = (tid >> 1) & 3;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 4;
+  uint64_t page = static_cast<uint64_t>(blockIdx.x) * 4 + (tid >> 6);
+  if (page >= n_pages) return;
+  const uint32_t base0 = smem_u32(&ring[0][tid * 4]);
+  constexpr uint32_t kStageBytes = 256 * 4 * 16;
+  auto issue = [&](int st, uint64_t pg) {
+    if (pg < n_pages) {
+      const uint4 *src = in + pg * 256 + b * 4;
+      const uint32_t dst = base0 + st * kStageBytes;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async16(dst + 16 * (c ^ sw), src + c);
+    }
+    cp_async_commit(); // empty groups keep the count uniform at the tail
+  };
+  issue(0, page);
+  issue(1, page + stride);
+  uint32_t k[8];
+  load_key(key, k);
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
+  uint32_t cached_hi = 0, cached_pid = 0;
+  bool cached = false;
+  int st = 0;
+  for (;;) {
+    issue(st == 0 ? 2 : st - 1, page + 2 * stride); // stage (st + 2) % 3
+    uint32_t s[4];
+    page_seed(desc, page, s);
+    if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+      cached_hi = s[1];
+      cached_pid = s[2];
+      cached = true;
+    }
+    uint32_t x[16];
+    x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
+    quarter_round<0>(x[0], x[4], x[8], x[12], rm);
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int r = 1; r < ROUNDS / 2; ++r) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    cp_async_wait<2>(); // this page's group has landed
+    const uint4 *mine = &ring[st][tid * 4];
+    const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
+    uint4 *dst = out + page * 256 + b * 4;
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]),
+                              d3.w ^ (x[15] + b)));
+    page += stride;
+    if (page >= n_pages) break;
+    st = st == 2 ? 0 : st + 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // Keystream only, arbitrary seeds: seeds[4*i .. 4*i+3] are state words 12..15
 // of block i; out[16*i ..] its 16 keystream words (block-major, like
 // _chacha_numba.keystream_words, _chacha_numba.py:45-50).

@@ -82,13 +82,14 @@ struct Tuning {
   std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
   std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
-  std::atomic<int> kernel{2};          // HBM kernel: 1 = k_crypt_blocks, 2 = k_crypt_pages,
-                                       // 3 = k_crypt_pages_coalesced, 4 = k_crypt_pages_tma
+  std::atomic<int> kernel{0};          // HBM kernel: 0 = auto (per rounds, below), 1 = k_crypt_blocks,
+                                       // 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced,
+                                       // 4 = k_crypt_pages_tma, 5 = k_crypt_pages_async
   std::atomic<int> host_mode{2};       // large host batches: 0 = round-robin streams, 1 = zero-copy kernel
                                        // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams
   std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
   Tuning() {
-    kernel = env_int("PAGECRYPT_KERNEL", 2);
+    kernel = env_int("PAGECRYPT_KERNEL", 0);
     host_mode = env_int("PAGECRYPT_HOST_MODE", 2);
     ctas_per_sm = env_int("PAGECRYPT_CTAS_PER_SM", 0);
     if (const char *v = std::getenv("PAGECRYPT_ROTMASK")) rot_mask = static_cast<uint32_t>(std::strtoul(v, nullptr, 0));
@@ -134,7 +135,7 @@ void launch_crypt_r(uint32_t mask, const uint32_t *key, const pc::PageDesc &d, c
 
 // Persistent grid for k_crypt_pages: SMs x resident CTAs (occupancy), capped
 // by the number of 4-page slots.
-template <int R, bool Coalesced>
+template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async
 unsigned pages_grid(size_t n_pages) {
   static int sms[64] = {0}, occ[64] = {0};
   int dev = 0;
@@ -143,8 +144,10 @@ unsigned pages_grid(size_t n_pages) {
   if (!sms[dev]) {
     cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
     int o = 0;
-    if constexpr (Coalesced)
+    if constexpr (Variant == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
+    else if constexpr (Variant == 2)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R>, 256, 0);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
     occ[dev] = o > 0 ? o : 1;
@@ -156,14 +159,16 @@ unsigned pages_grid(size_t n_pages) {
 }
 
 template <int R>
-void launch_pages_r(bool coalesced, const uint32_t *key, const pc::PageDesc &d, const void *in,
+void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const void *in,
                     void *out, size_t n_pages, cudaStream_t st) {
   auto i4 = static_cast<const uint4 *>(in);
   auto o4 = static_cast<uint4 *>(out);
-  if (coalesced)
-    pc::k_crypt_pages_coalesced<R><<<pages_grid<R, true>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
+  if (kern == 3)
+    pc::k_crypt_pages_coalesced<R><<<pages_grid<R, 1>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
+  else if (kern == 5)
+    pc::k_crypt_pages_async<R><<<pages_grid<R, 2>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
   else
-    pc::k_crypt_pages<R><<<pages_grid<R, false>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
+    pc::k_crypt_pages<R><<<pages_grid<R, 0>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
 }
 
 // ---- v4: TMA pipeline --------------------------------------------------------
@@ -231,12 +236,19 @@ int launch_tma_r(const uint32_t *key, const pc::PageDesc &d, const void *in, voi
   return PC_OK;
 }
 
-// kernel_override: 0 = the "kernel" knob, else force 1/2/3/4 (the zero-copy
+// Default kernel per round count, from the B200 sweeps in profiles/
+// (r01_kernel_sweep_*.txt, r01_clock_power_sweep.txt): ChaCha8 is HBM-bound
+// and wants the fully coalesced v3; ChaCha12/20 are ALU-bound and v5 (cp.async
+// ring, 4 CTAs/SM) is at least as fast as v2 there.
+int auto_kernel(int rounds) { return rounds == 8 ? 3 : 5; }
+
+// kernel_override: 0 = the "kernel" knob, else force 1..5 (the zero-copy
 // host path forces 3).
 int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out,
                  size_t n_pages, int rounds, cudaStream_t st, int kernel_override = 0) {
   if (n_pages == 0) return PC_OK;
-  const int kern = kernel_override ? kernel_override : tuning().kernel.load();
+  int kern = kernel_override ? kernel_override : tuning().kernel.load();
+  if (kern == 0) kern = auto_kernel(rounds);
   if (kern == 4) {
     switch (rounds) {
       case 8: return launch_tma_r<8>(key, d, in, out, n_pages, st);
@@ -244,11 +256,11 @@ int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, voi
       default: return launch_tma_r<20>(key, d, in, out, n_pages, st);
     }
   }
-  if (kern == 2 || kern == 3) {
+  if (kern == 2 || kern == 3 || kern == 5) {
     switch (rounds) {
-      case 8: launch_pages_r<8>(kern == 3, key, d, in, out, n_pages, st); break;
-      case 12: launch_pages_r<12>(kern == 3, key, d, in, out, n_pages, st); break;
-      default: launch_pages_r<20>(kern == 3, key, d, in, out, n_pages, st); break;
+      case 8: launch_pages_r<8>(kern, key, d, in, out, n_pages, st); break;
+      case 12: launch_pages_r<12>(kern, key, d, in, out, n_pages, st); break;
+      default: launch_pages_r<20>(kern, key, d, in, out, n_pages, st); break;
     }
     CU(cudaGetLastError());
     return PC_OK;
@@ -1313,7 +1325,7 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "kernel")) {
-    if (value < 1 || value > 4) return fail(PC_EINVAL, "kernel must be 1, 2, 3 or 4");
+    if (value < 0 || value > 5) return fail(PC_EINVAL, "kernel must be 0 (auto) or 1..5");
     t.kernel = static_cast<int>(value);
     return PC_OK;
   }

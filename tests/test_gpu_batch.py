@@ -53,7 +53,7 @@ def knob():
 
 
 class TestDevicePath:
-    @pytest.mark.parametrize("kernel", [1, 2, 3, 4])
+    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5])
     @pytest.mark.parametrize("rounds", [8, 12, 20])
     @pytest.mark.parametrize("n", [1, 3, 64, 4097])
     def test_contiguous_scalar_pid(self, dkey, n, rounds, kernel, knob):
@@ -66,7 +66,7 @@ class TestDevicePath:
         want = C.crypt_pages(KEY, None, None, pages, rounds=rounds, vaddr0=BASE, pid0=1, nthreads=8)
         assert np.array_equal(got.cpu().numpy(), want)
 
-    @pytest.mark.parametrize("kernel", [1, 2, 3, 4])
+    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5])
     def test_per_page_descriptors(self, dkey, ref_pages, kernel, knob):
         import torch
 
@@ -85,7 +85,7 @@ class TestDevicePath:
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), r["ct"])
 
-    @pytest.mark.parametrize("kernel", [1, 2, 3, 4])
+    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5])
     def test_pid_per_page_variant(self, dkey, kernel, knob):
         """pid = 1 + (i % 64); also vaddr_hi changing mid-batch
         (the v2/v3 kernels cache the vaddr_hi/pid column rounds)."""
