@@ -212,6 +212,10 @@ def main() -> None:
     ap.add_argument("--ref-pages", type=int, default=8192, help="reference arm: pages per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-extras", action="store_true", help="skip rounds 8/12 + latency sweeps")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="process-group backend for the barrier/max-time (gloo: test mode)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: every rank uses cuda:0 (multi-rank logic on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -230,10 +234,16 @@ def main() -> None:
     from paper_2004_09252_b200 import _native
     from paper_2004_09252_b200.partition import max_over_ranks, rank_pages
 
+    if args.same_device:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -274,7 +284,7 @@ def main() -> None:
 
     with ClockSampler(local_rank) as clk:
         total_ms = timed(args.rounds, args.steps, args.warmup)
-    t_max = max_over_ranks(total_ms, device=dev)
+    t_max = max_over_ranks(total_ms, device=red_dev)
     bytes_per_step = n * PAGE
     value = world * bytes_per_step * args.steps / (t_max / 1e3) / 1e9
     kernel_ms = total_ms / args.steps  # one launch per step
@@ -317,7 +327,7 @@ def main() -> None:
     for _ in range(e2e_steps):
         pc.crypt_pages(key, vaddr0, 1, host_in, out=host_out, rounds=args.rounds, engine=eng)
     e2e_s = time.perf_counter() - t0
-    e2e_s = max_over_ranks(e2e_s, device=dev)
+    e2e_s = max_over_ranks(e2e_s, device=red_dev)
     e2e = {"value": round(world * bytes_per_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": bytes_per_step, "d2h_bytes_per_step": bytes_per_step,
            "steps": e2e_steps, "path": "crypt_pages(DeviceKey, pinned torch CPU tensors) -> "
@@ -330,7 +340,7 @@ def main() -> None:
             if r == args.rounds:
                 continue
             ms = timed(r, max(5, args.steps // 2), 3) / max(5, args.steps // 2)
-            t = max_over_ranks(ms, device=dev)
+            t = max_over_ranks(ms, device=red_dev)
             extras[f"chacha{r}"] = {"value": round(world * bytes_per_step / (t / 1e3) / 1e9, 2),
                                     "unit": "GB/s", "roofline": roofline(r, ms)}
         if rank == 0:
