@@ -25,6 +25,7 @@
 #include "../../include/pagecrypt.h"
 #include "kernels.cuh"
 #include "service.cuh"
+#include "hostpool.hpp"
 
 namespace {
 
@@ -473,6 +474,7 @@ struct pc_engine {
   uint8_t *hd_small = nullptr;      // device alias of h_small (zero-copy)
   uint8_t *d_small = nullptr;
   size_t small_bytes = 0;
+  std::unique_ptr<pc::HostPool> pool; // pageable <-> pinned bounce copies (lazy)
 };
 
 // ===========================================================================
@@ -765,6 +767,10 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   if (!pin_in || !pin_out) {
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(cudaHostAlloc(&e->h_bounce[s], C * PC_PAGE_SIZE, cudaHostAllocDefault));
+    if (!e->pool) {
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      e->pool.reset(new pc::HostPool(std::min(7u, hw > 1 ? hw / 2 : 0u)));
+    }
   }
   // Chunk schedule: ramp up C/8, C/4, C/2 at the start and down at the end
   // (when the batch is large enough) so the pipeline fills and drains with
@@ -798,7 +804,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
     CU(cudaEventSynchronize(e->done[s]));
     if (!pin_out) {
       const size_t p0 = starts[c], m = starts[c + 1] - p0;
-      std::memcpy(dst_b + p0 * PC_PAGE_SIZE, e->h_bounce[s], m * PC_PAGE_SIZE);
+      e->pool->memcpy(dst_b + p0 * PC_PAGE_SIZE, e->h_bounce[s], m * PC_PAGE_SIZE);
     }
     return PC_OK;
   };
@@ -818,7 +824,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
     }
     const uint8_t *src = src_b + p0 * PC_PAGE_SIZE;
     if (!pin_in) {
-      std::memcpy(e->h_bounce[s], src, m * PC_PAGE_SIZE);
+      e->pool->memcpy(e->h_bounce[s], src, m * PC_PAGE_SIZE);
       src = e->h_bounce[s];
     }
     CU(cudaMemcpyAsync(e->d_pages[s], src, m * PC_PAGE_SIZE, cudaMemcpyHostToDevice, sh));
