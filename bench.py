@@ -346,6 +346,7 @@ def main() -> None:
         if rank == 0:
             extras["latency_host_small"] = latency_sweep(pc, key, local_rank)
             extras["latency_service_1page"] = service_latency(local_rank)
+            extras["hbm_store"] = store_throughput(pc, key, local_rank)
     del host_in, host_out
 
     cpu = None
@@ -413,6 +414,31 @@ def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
         res[str(n)] = {"p50_us": round(p50, 2), "p99_us": round(ts[int(len(ts) * 0.99)] / 1e3, 2),
                        "gbps_at_p50": round(n * PAGE / (p50 * 1e-6) / 1e9, 3)}
     return res
+
+
+def store_throughput(pc, key, device: int, n: int = 65536) -> dict:
+    """evict (encrypt into the HBM page store) and refault
+    (decrypt out of it) 256 MiB of pinned host pages in one batch each."""
+    import torch
+
+    from paper_2004_09252_b200.store import DevicePageStore
+    from paper_2004_09252_b200.workers import ClientId
+
+    st = DevicePageStore(n, key, device=device)
+    src = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8).pin_memory()
+    vaddrs = (np.arange(n, dtype=np.uint64) * np.uint64(PAGE) + np.uint64(BASE_VADDR))
+    c = ClientId(1, 0)
+    st.evict_many(c, vaddrs, src.numpy())  # warm-up
+    st.refault_many(c, vaddrs)
+    t0 = time.perf_counter()
+    st.evict_many(c, vaddrs, src.numpy())
+    t1 = time.perf_counter()
+    back = st.refault_many(c, vaddrs)
+    t2 = time.perf_counter()
+    ok = bool(np.array_equal(back, src.numpy()))
+    return {"pages": n, "evict_gbs": round(n * PAGE / (t1 - t0) / 1e9, 2),
+            "refault_gbs": round(n * PAGE / (t2 - t1) / 1e9, 2), "roundtrip_identical": ok,
+            "note": "pinned source, pageable refault destination"}
 
 
 def service_latency(device: int, reps: int = 2000) -> dict:

@@ -148,6 +148,21 @@ int pc_service_timing(pc_service *svc, int worker, uint64_t ticket, uint64_t out
 int pc_service_max_workers(int device, int *n);
 int pc_service_stop(pc_service *svc);
 
+/* ---- (viii) HBM page store (device-resident ciphertext) -----
+ * The B200 side of EncryptedPageStore (pkg/src/pagecrypt/store.py:41-105)
+ * with the ciphertext pages resident in a device slab of slab_pages pages.
+ * pc_slab_transfer moves n pages between host memory and slab slots
+ * slots[i]; dir 0 = host -> slab (evict / insert), 1 = slab -> host
+ * (refault / lookup).  With a key the page passes through the cipher on the
+ * way (encrypt on evict, decrypt on refault; vaddrs/pids or vaddr0/pid0 as
+ * in pc_crypt_pages_host), so plaintext never rests in HBM and ciphertext
+ * never crosses PCIe; with key == NULL the bytes are copied verbatim.
+ * Synchronous.  pc_slab_wipe zeroes freed slots (store.py:86-92). */
+int pc_slab_transfer(pc_engine *eng, const pc_key *key, void *slab, size_t slab_pages,
+                     const uint32_t *slots, const uint64_t *vaddrs, const uint32_t *pids,
+                     uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds);
+int pc_slab_wipe(pc_engine *eng, void *slab, size_t slab_pages, const uint32_t *slots, size_t n);
+
 /* ---- pinned host memory helpers --------------------------------------- */
 int pc_host_alloc(size_t bytes, void **out);
 int pc_host_free(void *p);

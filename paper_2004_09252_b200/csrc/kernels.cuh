@@ -469,6 +469,46 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
 }
 
 // ---------------------------------------------------------------------------
+// Slab moves for the HBM page store: page i of a staging batch <-> slot
+// slots[i] of a device slab, optionally through the cipher (key != nullptr).
+// DIR 0: staging -> slab (evict/insert), DIR 1: slab -> staging (refault/lookup).
+// One thread per 64-byte block, like v1; these moves are PCIe-bound.
+template <int ROUNDS, int DIR>
+__global__ void __launch_bounds__(256)
+k_slab_move(const uint32_t *__restrict__ key, PageDesc desc, const uint32_t *__restrict__ slots,
+            uint4 *slab, uint4 *staging, uint64_t n_blocks) {
+  const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n_blocks) return;
+  const uint64_t page = g >> 6;
+  const uint32_t blk = static_cast<uint32_t>(g & 63);
+  uint4 *sp = slab + static_cast<uint64_t>(__ldg(slots + page)) * 256 + blk * 4;
+  uint4 *tp = staging + g * 4;
+  const uint4 *src = DIR == 0 ? tp : sp;
+  uint4 *dst = DIR == 0 ? sp : tp;
+  uint4 d0 = ld_v4(src), d1 = ld_v4(src + 1), d2 = ld_v4(src + 2), d3 = ld_v4(src + 3);
+  if (key) {
+    uint32_t k[8], s[4], x[16];
+    load_key(key, k);
+    page_seed(desc, page, s);
+    s[3] = blk;
+    chacha_block<ROUNDS, 0>(x, k, s, RotMul{});
+    d0.x ^= x[0];  d0.y ^= x[1];  d0.z ^= x[2];  d0.w ^= x[3];
+    d1.x ^= x[4];  d1.y ^= x[5];  d1.z ^= x[6];  d1.w ^= x[7];
+    d2.x ^= x[8];  d2.y ^= x[9];  d2.z ^= x[10]; d2.w ^= x[11];
+    d3.x ^= x[12]; d3.y ^= x[13]; d3.z ^= x[14]; d3.w ^= x[15];
+  }
+  st_v4(dst, d0); st_v4(dst + 1, d1); st_v4(dst + 2, d2); st_v4(dst + 3, d3);
+}
+
+// Zero the given slab slots (freed store entries are wiped, store.py:86-92).
+__global__ void __launch_bounds__(256)
+k_slab_wipe(const uint32_t *__restrict__ slots, uint4 *slab, uint64_t n_chunks) {
+  const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n_chunks) return;
+  slab[static_cast<uint64_t>(__ldg(slots + (g >> 8))) * 256 + (g & 255)] = make_uint4(0, 0, 0, 0);
+}
+
+// ---------------------------------------------------------------------------
 // Keystream only, arbitrary seeds: seeds[4*i .. 4*i+3] are state words 12..15
 // of block i; out[16*i ..] its 16 keystream words (block-major, like
 // _chacha_numba.keystream_words, _chacha_numba.py:45-50).

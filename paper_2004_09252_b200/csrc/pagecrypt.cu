@@ -466,7 +466,7 @@ struct pc_engine {
   std::vector<uint64_t *> d_vaddrs; // per-stream descriptor staging
   std::vector<uint32_t *> d_pids;
   std::vector<uint8_t *> h_bounce;  // pinned bounce for pageable I/O (lazy)
-  std::vector<uint8_t *> h_desc;    // pinned descriptor staging (chunk*12 bytes)
+  std::vector<uint8_t *> h_desc;    // pinned descriptor staging (chunk*16 bytes)
   uint8_t *h_key = nullptr;         // pinned 256-B raw-key staging
   uint32_t *d_rawkey = nullptr;     // caller-key device slot (wiped after use)
   // small-batch path: one pinned+mapped region and its device mirror
@@ -638,8 +638,9 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
     CUE(cudaEventCreateWithFlags(&e->ev_k[s], cudaEventDisableTiming));
     CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_pages[s]), chunk_pages * PC_PAGE_SIZE, e->streams[0]));
     CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_vaddrs[s]), chunk_pages * 8, e->streams[0]));
-    CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_pids[s]), chunk_pages * 4, e->streams[0]));
-    CUE(cudaHostAlloc(&e->h_desc[s], chunk_pages * 12, cudaHostAllocDefault));
+    // d_pids: pids at [0, C), slab slots at [C, 2C); h_desc: vaddrs, pids, slots
+    CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_pids[s]), chunk_pages * 8, e->streams[0]));
+    CUE(cudaHostAlloc(&e->h_desc[s], chunk_pages * 16, cudaHostAllocDefault));
   }
   CUE(cudaHostAlloc(&e->h_key, 256, cudaHostAllocDefault));
   CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_rawkey), 256, e->streams[0]));
@@ -904,6 +905,148 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
   return rc;
 }
 
+} // extern "C"
+
+// ---- (viii) HBM page store: slab moves ------------------------------------------
+namespace {
+template <int R>
+void launch_slab_r(int dir, const uint32_t *key, const pc::PageDesc &d, const uint32_t *slots, void *slab,
+                   void *staging, size_t n, cudaStream_t st) {
+  const uint64_t nb = static_cast<uint64_t>(n) * 64;
+  const dim3 grid(static_cast<unsigned>((nb + 255) / 256));
+  auto sl = static_cast<uint4 *>(slab);
+  auto sg = static_cast<uint4 *>(staging);
+  if (dir == 0) pc::k_slab_move<R, 0><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb);
+  else pc::k_slab_move<R, 1><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb);
+}
+} // namespace
+
+extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, size_t slab_pages,
+                                const uint32_t *slots, const uint64_t *vaddrs, const uint32_t *pids,
+                                uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds) {
+  if (!e || e->magic != kEngineMagic) return fail(PC_ESTATE, "not a live pc_engine");
+  if (key && (key->magic != kKeyMagic || key->device != e->device))
+    return fail(PC_ESTATE, "key is not live or not on the engine's device");
+  if (dir != 0 && dir != 1) return fail(PC_EINVAL, "dir must be 0 (host->slab) or 1 (slab->host)");
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  if (n == 0) return PC_OK;
+  if (!slab || !slots || !host) return fail(PC_EINVAL, "slab/slots/host is NULL");
+  if (reinterpret_cast<uintptr_t>(slab) & 15) return fail(PC_EINVAL, "slab must be 16-byte aligned");
+  for (size_t i = 0; i < n; ++i)
+    if (slots[i] >= slab_pages) return fail(PC_EINVAL, "slot %u outside the %zu-page slab", slots[i], slab_pages);
+  if (key && !vaddrs && (vaddr0 & 4095)) return fail(PC_EINVAL, "vaddr0 not page-aligned");
+  if (key && vaddrs)
+    for (size_t i = 0; i < n; ++i)
+      if (vaddrs[i] & 4095) return fail(PC_EINVAL, "vaddr %#llx not page-aligned", (unsigned long long)vaddrs[i]);
+  std::lock_guard<std::mutex> lk(e->mu);
+  DeviceGuard g(e->device);
+  CU(g.err);
+  void *host_dev = nullptr;
+  const bool pinned = pinned_alias(host, &host_dev);
+  const int S = e->n_streams;
+  const size_t C = e->chunk_pages;
+  if (!pinned) {
+    for (int s = 0; s < S; ++s)
+      if (!e->h_bounce[s]) CU(cudaHostAlloc(&e->h_bounce[s], C * PC_PAGE_SIZE, cudaHostAllocDefault));
+    if (!e->pool) {
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      e->pool.reset(new pc::HostPool(std::min(7u, hw > 1 ? hw / 2 : 0u)));
+    }
+  }
+  auto *hb = static_cast<uint8_t *>(host);
+  const size_t n_chunks = (n + C - 1) / C;
+  auto finish = [&](size_t c) -> int { // wait for chunk c; deliver bounce -> host for gets
+    const int s = static_cast<int>(c % S);
+    CU(cudaEventSynchronize(e->done[s]));
+    if (dir == 1 && !pinned) {
+      const size_t p0 = c * C, m = std::min(C, n - p0);
+      e->pool->memcpy(hb + p0 * PC_PAGE_SIZE, e->h_bounce[s], m * PC_PAGE_SIZE);
+      wipe(e->h_bounce[s], m * PC_PAGE_SIZE); // plaintext left the pipeline
+    }
+    return PC_OK;
+  };
+  for (size_t c = 0; c < n_chunks; ++c) {
+    const int s = static_cast<int>(c % S);
+    cudaStream_t st = e->streams[s];
+    const size_t p0 = c * C, m = std::min(C, n - p0);
+    if (c >= static_cast<size_t>(S)) {
+      int rc = finish(c - S);
+      if (rc != PC_OK) return rc;
+    }
+    uint8_t *hd = e->h_desc[s];
+    std::memcpy(hd + C * 12, slots + p0, m * 4);
+    uint32_t *d_slots = e->d_pids[s] + C;
+    CU(cudaMemcpyAsync(d_slots, hd + C * 12, m * 4, cudaMemcpyHostToDevice, st));
+    pc::PageDesc d{nullptr, nullptr, vaddr0 + 4096ull * p0, pid0};
+    if (key && vaddrs) {
+      std::memcpy(hd, vaddrs + p0, m * 8);
+      CU(cudaMemcpyAsync(e->d_vaddrs[s], hd, m * 8, cudaMemcpyHostToDevice, st));
+      d.vaddrs = e->d_vaddrs[s];
+    }
+    if (key && pids) {
+      std::memcpy(hd + C * 8, pids + p0, m * 4);
+      CU(cudaMemcpyAsync(e->d_pids[s], hd + C * 8, m * 4, cudaMemcpyHostToDevice, st));
+      d.pids = e->d_pids[s];
+    }
+    uint8_t *staging = e->d_pages[s];
+    if (dir == 0) {
+      const uint8_t *src = hb + p0 * PC_PAGE_SIZE;
+      if (!pinned) {
+        e->pool->memcpy(e->h_bounce[s], src, m * PC_PAGE_SIZE);
+        src = e->h_bounce[s];
+      }
+      CU(cudaMemcpyAsync(staging, src, m * PC_PAGE_SIZE, cudaMemcpyHostToDevice, st));
+    }
+    const uint32_t *k = key ? key->d_words : nullptr;
+    switch (rounds) {
+      case 8: launch_slab_r<8>(dir, k, d, d_slots, slab, staging, m, st); break;
+      case 12: launch_slab_r<12>(dir, k, d, d_slots, slab, staging, m, st); break;
+      default: launch_slab_r<20>(dir, k, d, d_slots, slab, staging, m, st); break;
+    }
+    CU(cudaGetLastError());
+    if (dir == 1) {
+      uint8_t *dst = pinned ? hb + p0 * PC_PAGE_SIZE : e->h_bounce[s];
+      CU(cudaMemcpyAsync(dst, staging, m * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, st));
+    }
+    // the staging slot held plaintext (evict input / refault output): zero it
+    CU(cudaMemsetAsync(staging, 0, m * PC_PAGE_SIZE, st));
+    CU(cudaEventRecord(e->done[s], st));
+  }
+  const size_t first = n_chunks > static_cast<size_t>(S) ? n_chunks - S : 0;
+  for (size_t c = first; c < n_chunks; ++c) {
+    int rc = finish(c);
+    if (rc != PC_OK) return rc;
+  }
+  if (dir == 0 && !pinned)
+    for (int s = 0; s < S; ++s) wipe(e->h_bounce[s], std::min(C, n) * PC_PAGE_SIZE);
+  return PC_OK;
+}
+
+extern "C" int pc_slab_wipe(pc_engine *e, void *slab, size_t slab_pages, const uint32_t *slots, size_t n) {
+  if (!e || e->magic != kEngineMagic) return fail(PC_ESTATE, "not a live pc_engine");
+  if (n == 0) return PC_OK;
+  if (!slab || !slots) return fail(PC_EINVAL, "slab/slots is NULL");
+  for (size_t i = 0; i < n; ++i)
+    if (slots[i] >= slab_pages) return fail(PC_EINVAL, "slot %u outside the %zu-page slab", slots[i], slab_pages);
+  std::lock_guard<std::mutex> lk(e->mu);
+  DeviceGuard g(e->device);
+  CU(g.err);
+  cudaStream_t st = e->streams[0];
+  const size_t C = e->chunk_pages;
+  for (size_t p0 = 0; p0 < n; p0 += C) {
+    const size_t m = std::min(C, n - p0);
+    std::memcpy(e->h_desc[0] + C * 12, slots + p0, m * 4);
+    uint32_t *d_slots = e->d_pids[0] + C;
+    CU(cudaMemcpyAsync(d_slots, e->h_desc[0] + C * 12, m * 4, cudaMemcpyHostToDevice, st));
+    const uint64_t chunks = static_cast<uint64_t>(m) * 256;
+    pc::k_slab_wipe<<<static_cast<unsigned>((chunks + 255) / 256), 256, 0, st>>>(d_slots, static_cast<uint4 *>(slab), chunks);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st)); // h_desc[0] is reused by the next piece
+  }
+  return PC_OK;
+}
+
+extern "C" {
 // ---- (vi) multi-device partition --------------------------------------------
 int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, int n_dev,
                          const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0, uint32_t pid0,
