@@ -390,32 +390,44 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int ROUNDS>
+//
+// CONTIG specialises the common bulk case -- contiguous vaddrs (vaddr0 +
+// 4096*i) and one pid -- so that the page loop only carries 32-bit page
+// indices, pointers and the vaddr advance by constant strides, and the pid
+// column round is hoisted out of the loop entirely; the general case reads
+// per-page descriptors.  Page counts are < 2^31 (the host splits larger
+// batches).
+template <int ROUNDS, bool CONTIG>
 __global__ void __launch_bounds__(256, 4)
 k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
-                    uint64_t n_pages) {
+                    uint32_t n_pages) {
   constexpr RotMul rm{};
   constexpr int kStages = 3;
   __shared__ uint4 ring[kStages][256 * 4]; // 16 KiB per stage
   const uint32_t tid = threadIdx.x;
   const uint32_t b = tid & 63;
   const uint32_t sw = (tid >> 1) & 3;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * 4;
-  uint64_t page = static_cast<uint64_t>(blockIdx.x) * 4 + (tid >> 6);
+  const uint32_t stride = gridDim.x * 4;
+  uint32_t page = blockIdx.x * 4 + (tid >> 6);
   if (page >= n_pages) return;
   const uint32_t base0 = smem_u32(&ring[0][tid * 4]);
   constexpr uint32_t kStageBytes = 256 * 4 * 16;
-  auto issue = [&](int st, uint64_t pg) {
-    if (pg < n_pages) {
-      const uint4 *src = in + pg * 256 + b * 4;
-      const uint32_t dst = base0 + st * kStageBytes;
+  const uint64_t step = static_cast<uint64_t>(stride) * 256; // uint4 per stride
+  const uint4 *src_ahead = in + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint4 *dst = out + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint32_t page_ahead = page;
+  auto issue = [&](int st) { // next page for the ring, then advance the ahead cursor
+    if (page_ahead < n_pages) {
+      const uint32_t sdst = base0 + st * kStageBytes;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) cp_async16(dst + 16 * (c ^ sw), src + c);
+      for (int c = 0; c < 4; ++c) cp_async16(sdst + 16 * (c ^ sw), src_ahead + c);
     }
     cp_async_commit(); // empty groups keep the count uniform at the tail
+    page_ahead += stride;
+    src_ahead += step;
   };
-  issue(0, page);
-  issue(1, page + stride);
+  issue(0);
+  issue(1);
   uint32_t k[8];
   load_key(key, k);
   uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
@@ -423,19 +435,39 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
   uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
   uint32_t cached_hi = 0, cached_pid = 0;
   bool cached = false;
+  uint64_t va = desc.vaddr0 + (static_cast<uint64_t>(page) << 12);
+  const uint64_t va_step = static_cast<uint64_t>(stride) << 12;
+  if constexpr (CONTIG) {
+    c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = desc.pid0;
+    quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+  }
   int st = 0;
   for (;;) {
-    issue(st == 0 ? 2 : st - 1, page + 2 * stride); // stage (st + 2) % 3
-    uint32_t s[4];
-    page_seed(desc, page, s);
-    if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
-      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
-      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
-      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
-      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
-      cached_hi = s[1];
-      cached_pid = s[2];
-      cached = true;
+    issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
+    uint32_t s[3];
+    if constexpr (CONTIG) {
+      s[0] = static_cast<uint32_t>(va);
+      s[1] = static_cast<uint32_t>(va >> 32);
+      s[2] = desc.pid0;
+      if (!cached || s[1] != cached_hi) {
+        c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+        quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+        cached_hi = s[1];
+        cached = true;
+      }
+    } else {
+      uint32_t sd[4];
+      page_seed(desc, page, sd);
+      s[0] = sd[0]; s[1] = sd[1]; s[2] = sd[2];
+      if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
+        c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+        quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+        c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+        quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+        cached_hi = s[1];
+        cached_pid = s[2];
+        cached = true;
+      }
     }
     uint32_t x[16];
     x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
@@ -452,7 +484,6 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     cp_async_wait<2>(); // this page's group has landed
     const uint4 *mine = &ring[st][tid * 4];
     const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
-    uint4 *dst = out + page * 256 + b * 4;
     st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
                           d0.w ^ (x[3] + kSigma3)));
     st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
@@ -463,6 +494,8 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
                               d3.w ^ (x[15] + b)));
     page += stride;
     if (page >= n_pages) break;
+    dst += step;
+    va += va_step;
     st = st == 2 ? 0 : st + 1;
   }
   cp_async_wait<0>();

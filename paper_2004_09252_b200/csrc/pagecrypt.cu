@@ -148,7 +148,7 @@ unsigned pages_grid(size_t n_pages) {
     if constexpr (Variant == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
     else if constexpr (Variant == 2)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R, true>, 256, 0);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
     occ[dev] = o > 0 ? o : 1;
@@ -166,8 +166,20 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
   auto o4 = static_cast<uint4 *>(out);
   if (kern == 3)
     pc::k_crypt_pages_coalesced<R><<<pages_grid<R, 1>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
-  else if (kern == 5)
-    pc::k_crypt_pages_async<R><<<pages_grid<R, 2>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
+  else if (kern == 5) {
+    // 32-bit page loop: split batches at 2^30 pages (4 TiB)
+    constexpr size_t kMax = size_t(1) << 30;
+    for (size_t p0 = 0; p0 < n_pages; p0 += kMax) {
+      const uint32_t m = static_cast<uint32_t>(std::min(kMax, n_pages - p0));
+      pc::PageDesc dd{d.vaddrs ? d.vaddrs + p0 : nullptr, d.pids ? d.pids + p0 : nullptr,
+                      d.vaddr0 + 4096ull * p0, d.pid0};
+      const unsigned grid = pages_grid<R, 2>(m);
+      if (!dd.vaddrs && !dd.pids)
+        pc::k_crypt_pages_async<R, true><<<grid, 256, 0, st>>>(key, dd, i4 + p0 * 256, o4 + p0 * 256, m);
+      else
+        pc::k_crypt_pages_async<R, false><<<grid, 256, 0, st>>>(key, dd, i4 + p0 * 256, o4 + p0 * 256, m);
+    }
+  }
   else
     pc::k_crypt_pages<R><<<pages_grid<R, 0>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
 }
