@@ -157,10 +157,14 @@ int pc_service_stop(pc_service *svc);
  * way (encrypt on evict, decrypt on refault; vaddrs/pids or vaddr0/pid0 as
  * in pc_crypt_pages_host), so plaintext never rests in HBM and ciphertext
  * never crosses PCIe; with key == NULL the bytes are copied verbatim.
- * Synchronous.  pc_slab_wipe zeroes freed slots (store.py:86-92). */
+ * Synchronous.  flags PC_SLAB_WIPE_SRC (dir 1): zero each slot as it is
+ * read (a refault frees it).  pc_slab_wipe zeroes freed slots
+ * (store.py:86-92). */
+#define PC_SLAB_WIPE_SRC 1
 int pc_slab_transfer(pc_engine *eng, const pc_key *key, void *slab, size_t slab_pages,
                      const uint32_t *slots, const uint64_t *vaddrs, const uint32_t *pids,
-                     uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds);
+                     uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds,
+                     int flags);
 int pc_slab_wipe(pc_engine *eng, void *slab, size_t slab_pages, const uint32_t *slots, size_t n);
 
 /* ---- pinned host memory helpers --------------------------------------- */

@@ -58,7 +58,7 @@ SIGNATURES = {
     "pc_service_max_workers": (c_int, [c_int, P(c_int)]),
     "pc_service_stop": (c_int, [c_void_p]),
     "pc_slab_transfer": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
-                                 c_u64, c_u32, c_void_p, c_size_t, c_int, c_int]),
+                                 c_u64, c_u32, c_void_p, c_size_t, c_int, c_int, c_int]),
     "pc_slab_wipe": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t]),
     "pc_host_alloc": (c_int, [c_size_t, P(c_void_p)]),
     "pc_host_free": (c_int, [c_void_p]),

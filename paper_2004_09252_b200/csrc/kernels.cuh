@@ -509,7 +509,7 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
 template <int ROUNDS, int DIR>
 __global__ void __launch_bounds__(256)
 k_slab_move(const uint32_t *__restrict__ key, PageDesc desc, const uint32_t *__restrict__ slots,
-            uint4 *slab, uint4 *staging, uint64_t n_blocks) {
+            uint4 *slab, uint4 *staging, uint64_t n_blocks, bool wipe_src) {
   const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= n_blocks) return;
   const uint64_t page = g >> 6;
@@ -519,6 +519,10 @@ k_slab_move(const uint32_t *__restrict__ key, PageDesc desc, const uint32_t *__r
   const uint4 *src = DIR == 0 ? tp : sp;
   uint4 *dst = DIR == 0 ? sp : tp;
   uint4 d0 = ld_v4(src), d1 = ld_v4(src + 1), d2 = ld_v4(src + 2), d3 = ld_v4(src + 3);
+  if (DIR == 1 && wipe_src) { // refault: the slot is freed, zero it on the way out
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    st_v4(sp, z); st_v4(sp + 1, z); st_v4(sp + 2, z); st_v4(sp + 3, z);
+  }
   if (key) {
     uint32_t k[8], s[4], x[16];
     load_key(key, k);

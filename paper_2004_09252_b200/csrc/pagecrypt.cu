@@ -923,20 +923,22 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
 namespace {
 template <int R>
 void launch_slab_r(int dir, const uint32_t *key, const pc::PageDesc &d, const uint32_t *slots, void *slab,
-                   void *staging, size_t n, cudaStream_t st) {
+                   void *staging, size_t n, bool wipe_src, cudaStream_t st) {
   const uint64_t nb = static_cast<uint64_t>(n) * 64;
   const dim3 grid(static_cast<unsigned>((nb + 255) / 256));
   auto sl = static_cast<uint4 *>(slab);
   auto sg = static_cast<uint4 *>(staging);
-  if (dir == 0) pc::k_slab_move<R, 0><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb);
-  else pc::k_slab_move<R, 1><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb);
+  if (dir == 0) pc::k_slab_move<R, 0><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb, false);
+  else pc::k_slab_move<R, 1><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb, wipe_src);
 }
 } // namespace
 
 extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, size_t slab_pages,
                                 const uint32_t *slots, const uint64_t *vaddrs, const uint32_t *pids,
-                                uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds) {
+                                uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds,
+                                int flags) {
   if (!e || e->magic != kEngineMagic) return fail(PC_ESTATE, "not a live pc_engine");
+  const bool wipe_src = (flags & PC_SLAB_WIPE_SRC) != 0;
   if (key && (key->magic != kKeyMagic || key->device != e->device))
     return fail(PC_ESTATE, "key is not live or not on the engine's device");
   if (dir != 0 && dir != 1) return fail(PC_EINVAL, "dir must be 0 (host->slab) or 1 (slab->host)");
@@ -1011,9 +1013,9 @@ extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, siz
     }
     const uint32_t *k = key ? key->d_words : nullptr;
     switch (rounds) {
-      case 8: launch_slab_r<8>(dir, k, d, d_slots, slab, staging, m, st); break;
-      case 12: launch_slab_r<12>(dir, k, d, d_slots, slab, staging, m, st); break;
-      default: launch_slab_r<20>(dir, k, d, d_slots, slab, staging, m, st); break;
+      case 8: launch_slab_r<8>(dir, k, d, d_slots, slab, staging, m, wipe_src, st); break;
+      case 12: launch_slab_r<12>(dir, k, d, d_slots, slab, staging, m, wipe_src, st); break;
+      default: launch_slab_r<20>(dir, k, d, d_slots, slab, staging, m, wipe_src, st); break;
     }
     CU(cudaGetLastError());
     if (dir == 1) {

@@ -24,6 +24,8 @@ Only ``client.pid`` enters the cipher seed, as in the reference worker
 
 from __future__ import annotations
 
+from collections import deque
+
 import numpy as np
 
 from . import _native
@@ -53,21 +55,30 @@ class DevicePageStore:
         self._engine = engine or default_engine(device)
         self._slab = torch.zeros((capacity_pages, PAGE_SIZE), dtype=torch.uint8, device=f"cuda:{device}")
         torch.cuda.synchronize(device)
-        self._free = list(range(capacity_pages - 1, -1, -1))
+        # free-slot stack: _free_arr[:_nfree] are free (top = lowest slots first)
+        self._free_arr = np.arange(capacity_pages - 1, -1, -1, dtype=np.uint32)
+        self._nfree = capacity_pages
         self._clients: dict[object, dict[int, int]] = {}
 
     # -- bookkeeping -------------------------------------------------------
 
     @property
     def free_slots(self) -> int:
-        return len(self._free)
+        return self._nfree
 
-    def _take(self, n: int) -> list[int]:
-        if n > len(self._free):
-            raise StoreFull(f"need {n} slots, {len(self._free)} free of {self.capacity}")
-        return [self._free.pop() for _ in range(n)]
+    def _take(self, n: int) -> np.ndarray:
+        if n > self._nfree:
+            raise StoreFull(f"need {n} slots, {self._nfree} free of {self.capacity}")
+        self._nfree -= n
+        return self._free_arr[self._nfree:self._nfree + n][::-1].copy()
 
-    def _move(self, slots, host: np.ndarray, direction: int, vaddrs=None, pid: int = 0, cipher: bool = False):
+    def _release(self, slots) -> None:
+        sl = np.asarray(slots, dtype=np.uint32)
+        self._free_arr[self._nfree:self._nfree + sl.size] = sl
+        self._nfree += sl.size
+
+    def _move(self, slots, host: np.ndarray, direction: int, vaddrs=None, pid: int = 0, cipher: bool = False,
+              wipe_src: bool = False):
         sl = np.ascontiguousarray(slots, dtype=np.uint32)
         va = None
         if cipher:
@@ -77,7 +88,7 @@ class DevicePageStore:
         _native.call("pc_slab_transfer", self._engine.handle, self.key.handle if cipher else None,
                      self._slab.data_ptr(), self.capacity, sl.ctypes.data,
                      None if va is None else va.ctypes.data, None, 0, pid & 0xFFFFFFFF,
-                     host.ctypes.data, sl.size, direction, self.rounds)
+                     host.ctypes.data, sl.size, direction, self.rounds, 1 if wipe_src else 0)
 
     def _wipe(self, slots) -> None:
         sl = np.ascontiguousarray(slots, dtype=np.uint32)
@@ -101,13 +112,13 @@ class DevicePageStore:
         sub = self._clients.setdefault(client, {})
         if vaddr in sub:
             raise ContractViolation(f"duplicate store insert for {client} {vaddr:#x}")
-        (slot,) = self._take(1)
+        slot = self._take(1)
         try:
-            self._move([slot], arr, 0)
+            self._move(slot, arr, 0)
         except Exception:
-            self._free.append(slot)
+            self._release(slot)
             raise
-        sub[vaddr] = slot
+        sub[vaddr] = int(slot[0])
 
     def lookup(self, client, vaddr: int):
         """Ciphertext bytes if present, else None (a first touch)."""
@@ -125,7 +136,7 @@ class DevicePageStore:
             raise ContractViolation(f"no store entry for {client} {vaddr:#x}")
         slot = sub.pop(vaddr)
         self._wipe([slot])
-        self._free.append(slot)
+        self._release([slot])
 
     def contains(self, client, vaddr: int) -> bool:
         return vaddr in self._clients.get(client, {})
@@ -135,9 +146,9 @@ class DevicePageStore:
         sub = self._clients.pop(client, None)
         if not sub:
             return
-        slots = list(sub.values())
+        slots = np.fromiter(sub.values(), dtype=np.uint32, count=len(sub))
         self._wipe(slots)
-        self._free.extend(slots)
+        self._release(slots)
 
     def pages(self, client):
         """(vaddr, ciphertext) in strictly increasing vaddr order."""
@@ -164,37 +175,41 @@ class DevicePageStore:
         return self.refault_many(client, [vaddr])[0].tobytes()
 
     def evict_many(self, client, vaddrs, plains) -> None:
-        vaddrs = [int(v) for v in vaddrs]
-        for v in vaddrs:
-            _check_vaddr_int(v)
+        va, _ = _host_vaddrs(np.asarray(vaddrs) if not isinstance(vaddrs, (list, tuple)) else vaddrs,
+                             len(vaddrs))
         arr = np.ascontiguousarray(plains, dtype=np.uint8).reshape(-1, PAGE_SIZE)
-        if arr.shape[0] != len(vaddrs):
-            raise ContractViolation(f"{len(vaddrs)} vaddrs for {arr.shape[0]} pages")
+        if arr.shape[0] != va.size:
+            raise ContractViolation(f"{va.size} vaddrs for {arr.shape[0]} pages")
+        vlist = va.tolist()
+        vset = set(vlist)
         sub = self._clients.setdefault(client, {})
-        if len(set(vaddrs)) != len(vaddrs) or any(v in sub for v in vaddrs):
+        if len(vset) != len(vlist) or not vset.isdisjoint(sub.keys()):
             raise ContractViolation("duplicate store insert")
-        slots = self._take(len(vaddrs))
+        slots = self._take(len(vlist))
         try:
-            self._move(slots, arr, 0, vaddrs=vaddrs, pid=client.pid, cipher=True)
+            self._move(slots, arr, 0, vaddrs=va, pid=client.pid, cipher=True)
         except Exception:
-            self._free.extend(slots)
+            self._release(slots)
             raise
-        for v, s in zip(vaddrs, slots):
-            sub[v] = s
+        sub.update(zip(vlist, slots.tolist()))
 
-    def refault_many(self, client, vaddrs) -> np.ndarray:
-        vaddrs = [int(v) for v in vaddrs]
+    def refault_many(self, client, vaddrs, out: np.ndarray | None = None) -> np.ndarray:
+        va, _ = _host_vaddrs(np.asarray(vaddrs) if not isinstance(vaddrs, (list, tuple)) else vaddrs,
+                             len(vaddrs))
+        vlist = va.tolist()
         sub = self._clients.get(client, {})
-        missing = [v for v in vaddrs if v not in sub]
-        if missing:
-            raise ContractViolation(f"no store entry for {client} {missing[0]:#x}")
-        if len(set(vaddrs)) != len(vaddrs):
+        if len(set(vlist)) != len(vlist):
             raise ContractViolation("duplicate vaddr in refault batch")
-        slots = [sub[v] for v in vaddrs]
-        out = np.empty((len(vaddrs), PAGE_SIZE), dtype=np.uint8)
-        self._move(slots, out, 1, vaddrs=vaddrs, pid=client.pid, cipher=True)
-        for v in vaddrs:
-            del sub[v]
-        self._wipe(slots)
-        self._free.extend(slots)
+        try:
+            slots = np.fromiter(map(sub.__getitem__, vlist), dtype=np.uint32, count=len(vlist))
+        except KeyError as exc:
+            raise ContractViolation(f"no store entry for {client} {exc.args[0]:#x}") from None
+        if out is None:
+            out = np.empty((len(vlist), PAGE_SIZE), dtype=np.uint8)
+        elif out.nbytes != len(vlist) * PAGE_SIZE or not out.flags.c_contiguous:
+            raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
+        # decrypt on the way out and zero each slot as it is read (freed)
+        self._move(slots, out, 1, vaddrs=va, pid=client.pid, cipher=True, wipe_src=True)
+        deque(map(sub.pop, vlist), maxlen=0)
+        self._release(slots)
         return out

@@ -296,3 +296,36 @@ def test_scanner_positive_control(cuda):
     leak = bytearray(a ^ b for a, b in zip(masked, mask))
     assert _scan_process_memory([a ^ b for a, b in zip(masked, mask)]) >= 1
     leak[:] = bytes(32)
+
+
+def test_service_coexists_with_bulk_work_and_lifecycles(cuda):
+    """A persistent service kernel must not deadlock the rest of the library:
+    no entry point may device-synchronise (key install/destroy, engine
+    create/destroy, store create/wipe, bulk crypt on other streams)."""
+    import torch
+
+    import paper_2004_09252_b200 as pc
+    from paper_2004_09252_b200.store import DevicePageStore
+
+    pool = make_pool(4)
+    try:
+        for _ in range(3):
+            k = pc.DeviceKey.install(KEY, 0)
+            pages = torch.randint(0, 256, (2048, PAGE_SIZE), dtype=torch.uint8, device="cuda")
+            ct = pc.crypt_pages(k, 0x1000, 1, pages)
+            back = pc.crypt_pages(k, 0x1000, 1, ct)
+            assert torch.equal(back, pages)
+            eng = pc.Engine(0, n_streams=2, chunk_pages=256)
+            host = np.random.default_rng(0).integers(0, 256, size=(600, PAGE_SIZE), dtype=np.uint8)
+            assert np.array_equal(pc.crypt_pages(k, 0x1000, 1, pc.crypt_pages(k, 0x1000, 1, host, engine=eng),
+                                                 engine=eng), host)
+            eng.destroy()
+            st = DevicePageStore(16, k)
+            st.evict(ClientId(1, 0), 0x5000, bytes(PAGE_SIZE))
+            assert st.refault(ClientId(1, 0), 0x5000) == bytes(PAGE_SIZE)
+            k.destroy()
+            page = Page()
+            pool.crypt(ClientId(2, 0), 0x9000, "encrypt", page)
+            assert bytes(page.data) == O.crypt_page(KEY, 0x9000, 2, bytes(PAGE_SIZE))
+    finally:
+        pool.shutdown()

@@ -1,0 +1,69 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck,
+racecheck, synccheck): each page-kernel variant x rounds on ragged batches,
+in place and with per-page descriptors, the host paths, the keystream seams,
+the worker service and the HBM store.  Checks results against the oracle
+too, so a sanitizer run is also a parity run."""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2004_09252_b200 as pc  # noqa: E402
+from paper_2004_09252_b200 import _native  # noqa: E402
+from paper_2004_09252_b200.store import DevicePageStore  # noqa: E402
+from paper_2004_09252_b200.workers import ClientId, WorkerPool  # noqa: E402
+from oracle import coracle as C  # noqa: E402
+
+KEY = bytes(range(32))
+
+
+def main():
+    rng = np.random.default_rng(0)
+    n = 37
+    pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
+    va = (np.arange(n, dtype=np.uint64)[::-1] * np.uint64(4096) + np.uint64(0xFFFF_F000_0000)).copy()
+    pi = (np.arange(n) % 5).astype(np.uint32)
+    with pc.DeviceKey.install(KEY, 0) as k:
+        for kern in (1, 2, 3, 4, 5):
+            _native.tune("kernel", kern)
+            for r in (8, 20):
+                d = torch.from_numpy(pages).cuda()
+                pc.crypt_pages(k, 0x1_0000_0000, 3, d, out=d, rounds=r)
+                want = C.crypt_pages(KEY, None, None, pages, rounds=r, vaddr0=0x1_0000_0000, pid0=3)
+                assert np.array_equal(d.cpu().numpy(), want), (kern, r)
+                got = pc.crypt_pages(k, torch.from_numpy(va.view(np.int64)).cuda(),
+                                     torch.from_numpy(pi.view(np.int32)).cuda(), torch.from_numpy(pages).cuda(), rounds=r)
+                assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, va, pi, pages, rounds=r)), (kern, r)
+        _native.tune("kernel", 0)
+        for hm in (0, 1, 2):
+            _native.tune("host_mode", hm)
+            src = torch.from_numpy(np.concatenate([pages] * 3)).pin_memory()
+            out = torch.empty_like(src).pin_memory()
+            eng = pc.Engine(0, n_streams=3, chunk_pages=16)
+            pc.crypt_pages(k, 0x2000, 1, src, out=out, engine=eng)
+            eng.destroy()
+            assert np.array_equal(out.numpy(), C.crypt_pages(KEY, None, None, src.numpy(), vaddr0=0x2000, pid0=1))
+        _native.tune("host_mode", 2)
+        assert pc.crypt_page(KEY, 0x3000, 9, pages[0].tobytes()) == C.crypt_pages(KEY, [0x3000], 9, pages[:1])[0].tobytes()
+        assert pc.page_keystream(KEY, 0x3000, 9)[:64] == C.crypt_pages(KEY, [0x3000], 9, np.zeros((1, 4096), np.uint8))[0, :64].tobytes()
+        st = DevicePageStore(64, k)
+        st.evict_many(ClientId(5, 0), va[:20], pages[:20])
+        back = st.refault_many(ClientId(5, 0), va[:20])
+        assert np.array_equal(back, pages[:20])
+    pool = WorkerPool(n_workers=3, keysource=lambda m: KEY)
+    for i in range(12):
+        buf = bytearray(pages[i].tobytes())
+        pool.crypt(ClientId(7, 0), 4096 * i, "encrypt", type("P", (), {"data": buf})())
+        assert bytes(buf) == C.crypt_pages(KEY, [4096 * i], 7, pages[i:i + 1])[0].tobytes()
+    pool.shutdown()
+    torch.cuda.synchronize()
+    print("sanitize driver ok")
+
+
+if __name__ == "__main__":
+    main()
