@@ -39,6 +39,7 @@ extern "C" {
 #define PC_ENOMEM 3 /* device or pinned allocation failed */
 #define PC_ESTATE 4 /* object used after destroy, wrong device, ... */
 #define PC_ETIMEOUT 5 /* a service request did not complete in time */
+#define PC_EFULL 6    /* the HBM page store has no free slot for the batch */
 
 #define PC_PAGE_SIZE 4096
 #define PC_BLOCK_SIZE 64
@@ -166,6 +167,27 @@ int pc_slab_transfer(pc_engine *eng, const pc_key *key, void *slab, size_t slab_
                      uint64_t vaddr0, uint32_t pid0, void *host, size_t n, int dir, int rounds,
                      int flags);
 int pc_slab_wipe(pc_engine *eng, void *slab, size_t slab_pages, const uint32_t *slots, size_t n);
+
+/* The store itself: an HBM slab plus a native index client -> vaddr -> slot
+ * (the reference store's client -> SortedDict, store.py:41-51).  `client`
+ * is any 64-bit id (the Python layer uses pid << 32 | epoch); `pid` is what
+ * enters the cipher seed (workers.py:137).  put: evict (encrypt = 1) or
+ * insert verbatim ciphertext (0); duplicates or a full slab reject the whole
+ * batch (PC_EINVAL / PC_EFULL).  get: refault (decrypt = 1, remove = 1: slots
+ * zeroed as read and freed) or lookup (0, 0); missing entries -> PC_EINVAL.
+ * remove / drop_client wipe the freed slots.  list returns sorted vaddrs. */
+typedef struct pc_store pc_store;
+int pc_store_create(pc_engine *eng, const pc_key *key, size_t capacity_pages, int rounds, pc_store **out);
+int pc_store_destroy(pc_store *store);
+int pc_store_put(pc_store *store, uint64_t client, uint32_t pid, const uint64_t *vaddrs, size_t n,
+                 const void *host, int encrypt);
+int pc_store_get(pc_store *store, uint64_t client, uint32_t pid, const uint64_t *vaddrs, size_t n,
+                 void *host, int decrypt, int remove);
+int pc_store_remove(pc_store *store, uint64_t client, const uint64_t *vaddrs, size_t n);
+int pc_store_drop_client(pc_store *store, uint64_t client);
+int pc_store_contains(pc_store *store, uint64_t client, uint64_t vaddr, int *found);
+int pc_store_list(pc_store *store, uint64_t client, uint64_t *vaddrs, size_t cap, size_t *n);
+int pc_store_free_slots(pc_store *store, size_t *n);
 
 /* ---- pinned host memory helpers --------------------------------------- */
 int pc_host_alloc(size_t bytes, void **out);

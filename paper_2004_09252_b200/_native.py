@@ -22,7 +22,7 @@ from .errors import ContractViolation, NativeLibraryMissing, PageCryptError
 LIB_NAME = "libpagecrypt.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ESTATE, PC_ETIMEOUT = 0, 1, 2, 3, 4, 5
+PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ESTATE, PC_ETIMEOUT, PC_EFULL = 0, 1, 2, 3, 4, 5, 6
 
 c_void_p, c_size_t, c_int = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
 c_u32, c_u64 = ctypes.c_uint32, ctypes.c_uint64
@@ -60,6 +60,15 @@ SIGNATURES = {
     "pc_slab_transfer": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
                                  c_u64, c_u32, c_void_p, c_size_t, c_int, c_int, c_int]),
     "pc_slab_wipe": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t]),
+    "pc_store_create": (c_int, [c_void_p, c_void_p, c_size_t, c_int, P(c_void_p)]),
+    "pc_store_destroy": (c_int, [c_void_p]),
+    "pc_store_put": (c_int, [c_void_p, c_u64, c_u32, c_void_p, c_size_t, c_void_p, c_int]),
+    "pc_store_get": (c_int, [c_void_p, c_u64, c_u32, c_void_p, c_size_t, c_void_p, c_int, c_int]),
+    "pc_store_remove": (c_int, [c_void_p, c_u64, c_void_p, c_size_t]),
+    "pc_store_drop_client": (c_int, [c_void_p, c_u64]),
+    "pc_store_contains": (c_int, [c_void_p, c_u64, c_u64, P(c_int)]),
+    "pc_store_list": (c_int, [c_void_p, c_u64, c_void_p, c_size_t, P(c_size_t)]),
+    "pc_store_free_slots": (c_int, [c_void_p, P(c_size_t)]),
     "pc_host_alloc": (c_int, [c_size_t, P(c_void_p)]),
     "pc_host_free": (c_int, [c_void_p]),
     "pc_host_register": (c_int, [c_void_p, c_size_t]),

@@ -1519,3 +1519,5 @@ int pc_tune_get(const char *knob, int64_t *value) {
 }
 
 } // extern "C"
+
+#include "store.inc"

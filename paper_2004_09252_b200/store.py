@@ -1,9 +1,11 @@
 """HBM-resident encrypted page store.
 
 ``pagecrypt.store.EncryptedPageStore`` (``pkg/src/pagecrypt/store.py:41-105``)
-keeps one ciphertext copy per (client, vaddr) in host RAM.  Here the pages
-live in a device slab (``capacity_pages`` x 4 KiB of HBM; 180 GB holds ~44M
-pages) and only the index (client -> vaddr -> slot) is on the host.
+keeps one ciphertext copy per (client, vaddr) in host RAM under a
+client -> SortedDict index.  Here the pages live in a device slab
+(``capacity_pages`` x 4 KiB of HBM; 180 GB holds ~44M pages) and the index
+is native (``pc_store_*``, ``csrc/store.inc``), so batched calls spend their
+time on PCIe, not on per-page bookkeeping.
 
 Same API and errors as the reference store (``insert``/``lookup``/``remove``/
 ``contains``/``drop_client``/``pages``/``page_count``; ContractViolation for
@@ -19,17 +21,17 @@ slots are wiped), plus the fused paths the B200 makes possible:
   pipelined transfer per batch.
 
 Only ``client.pid`` enters the cipher seed, as in the reference worker
-(``workers.py:137``).
+(``workers.py:137``); the index is keyed by (pid, epoch).
 """
 
 from __future__ import annotations
 
-from collections import deque
+import ctypes
 
 import numpy as np
 
 from . import _native
-from .engine import DeviceKey, Engine, _check_vaddr_int, _host_vaddrs, default_engine
+from .engine import DeviceKey, Engine, _host_vaddrs, default_engine
 from .errors import ContractViolation, PageCryptError
 
 PAGE_SIZE = 4096
@@ -39,13 +41,13 @@ class StoreFull(PageCryptError):
     """No free slot left in the device slab."""
 
 
+def _cid(client) -> int:
+    return ((int(client.pid) & 0xFFFFFFFF) << 32) | (int(getattr(client, "epoch", 0)) & 0xFFFFFFFF)
+
+
 class DevicePageStore:
     def __init__(self, capacity_pages: int, key: DeviceKey | None = None, *, device: int = 0,
                  rounds: int = 20, engine: Engine | None = None):
-        import torch
-
-        if capacity_pages < 1 or capacity_pages >= 2**32:
-            raise ContractViolation("capacity_pages must be in 1..2^32-1")
         if key is not None and key.device != device:
             raise ContractViolation(f"key on device {key.device}, store on {device}")
         self.device = device
@@ -53,47 +55,36 @@ class DevicePageStore:
         self.rounds = rounds
         self.capacity = capacity_pages
         self._engine = engine or default_engine(device)
-        self._slab = torch.zeros((capacity_pages, PAGE_SIZE), dtype=torch.uint8, device=f"cuda:{device}")
-        torch.cuda.synchronize(device)
-        # free-slot stack: _free_arr[:_nfree] are free (top = lowest slots first)
-        self._free_arr = np.arange(capacity_pages - 1, -1, -1, dtype=np.uint32)
-        self._nfree = capacity_pages
-        self._clients: dict[object, dict[int, int]] = {}
+        self._lib = _native.load()
+        h = ctypes.c_void_p()
+        _native.call("pc_store_create", self._engine.handle, None if key is None else key.handle,
+                     capacity_pages, rounds, ctypes.byref(h))
+        self._h = h.value
+        self._clients = {}  # cid -> client object (for iteration helpers)
 
-    # -- bookkeeping -------------------------------------------------------
+    def _call(self, name, *args):
+        rc = getattr(self._lib, name)(*args)
+        if rc == _native.PC_EFULL:
+            raise StoreFull(self._lib.pc_last_error().decode())
+        _native.check(rc)
+
+    def close(self) -> None:
+        """Wipe the slab and free it."""
+        if self._h is not None:
+            h, self._h = self._h, None
+            _native.call("pc_store_destroy", h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     @property
     def free_slots(self) -> int:
-        return self._nfree
-
-    def _take(self, n: int) -> np.ndarray:
-        if n > self._nfree:
-            raise StoreFull(f"need {n} slots, {self._nfree} free of {self.capacity}")
-        self._nfree -= n
-        return self._free_arr[self._nfree:self._nfree + n][::-1].copy()
-
-    def _release(self, slots) -> None:
-        sl = np.asarray(slots, dtype=np.uint32)
-        self._free_arr[self._nfree:self._nfree + sl.size] = sl
-        self._nfree += sl.size
-
-    def _move(self, slots, host: np.ndarray, direction: int, vaddrs=None, pid: int = 0, cipher: bool = False,
-              wipe_src: bool = False):
-        sl = np.ascontiguousarray(slots, dtype=np.uint32)
-        va = None
-        if cipher:
-            if self.key is None:
-                raise PageCryptError("this store has no DeviceKey: use insert/lookup for ciphertext")
-            va, _ = _host_vaddrs(np.asarray(vaddrs, dtype=np.uint64), sl.size)
-        _native.call("pc_slab_transfer", self._engine.handle, self.key.handle if cipher else None,
-                     self._slab.data_ptr(), self.capacity, sl.ctypes.data,
-                     None if va is None else va.ctypes.data, None, 0, pid & 0xFFFFFFFF,
-                     host.ctypes.data, sl.size, direction, self.rounds, 1 if wipe_src else 0)
-
-    def _wipe(self, slots) -> None:
-        sl = np.ascontiguousarray(slots, dtype=np.uint32)
-        _native.call("pc_slab_wipe", self._engine.handle, self._slab.data_ptr(), self.capacity,
-                     sl.ctypes.data, sl.size)
+        n = ctypes.c_size_t()
+        _native.call("pc_store_free_slots", self._h, ctypes.byref(n))
+        return n.value
 
     @staticmethod
     def _page(buf) -> np.ndarray:
@@ -102,6 +93,12 @@ class DevicePageStore:
             raise ContractViolation(f"page must be {PAGE_SIZE} bytes")
         return np.ascontiguousarray(arr, dtype=np.uint8)
 
+    @staticmethod
+    def _vaddrs(vaddrs) -> np.ndarray:
+        v = vaddrs if isinstance(vaddrs, (list, tuple)) else np.asarray(vaddrs)
+        arr, _ = _host_vaddrs(v, len(v))
+        return arr
+
     # -- reference API (store.py:53-105) --------------------------------------
 
     def insert(self, client, vaddr: int, cipher) -> None:
@@ -109,62 +106,61 @@ class DevicePageStore:
         if vaddr % PAGE_SIZE:
             raise ContractViolation(f"vaddr {vaddr:#x} not page-aligned")
         arr = self._page(cipher)
-        sub = self._clients.setdefault(client, {})
-        if vaddr in sub:
-            raise ContractViolation(f"duplicate store insert for {client} {vaddr:#x}")
-        slot = self._take(1)
-        try:
-            self._move(slot, arr, 0)
-        except Exception:
-            self._release(slot)
-            raise
-        sub[vaddr] = int(slot[0])
+        va = np.array([vaddr], dtype=np.uint64)
+        self._call("pc_store_put", self._h, _cid(client), client.pid, va.ctypes.data, 1, arr.ctypes.data, 0)
 
     def lookup(self, client, vaddr: int):
         """Ciphertext bytes if present, else None (a first touch)."""
-        slot = self._clients.get(client, {}).get(vaddr)
-        if slot is None:
+        if not self.contains(client, vaddr):
             return None
         out = np.empty(PAGE_SIZE, dtype=np.uint8)
-        self._move([slot], out, 1)
+        va = np.array([vaddr], dtype=np.uint64)
+        self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, 1, out.ctypes.data, 0, 0)
         return out.tobytes()
 
     def remove(self, client, vaddr: int) -> None:
         """Delete an entry; the released slot is wiped before reuse."""
-        sub = self._clients.get(client)
-        if sub is None or vaddr not in sub:
-            raise ContractViolation(f"no store entry for {client} {vaddr:#x}")
-        slot = sub.pop(vaddr)
-        self._wipe([slot])
-        self._release([slot])
+        va = np.array([vaddr], dtype=np.uint64)
+        self._call("pc_store_remove", self._h, _cid(client), va.ctypes.data, 1)
 
     def contains(self, client, vaddr: int) -> bool:
-        return vaddr in self._clients.get(client, {})
+        f = ctypes.c_int()
+        _native.call("pc_store_contains", self._h, _cid(client), int(vaddr) & (2**64 - 1), ctypes.byref(f))
+        return bool(f.value)
 
     def drop_client(self, client) -> None:
         """Remove and wipe every entry of a client.  Unknown client: no-op."""
-        sub = self._clients.pop(client, None)
-        if not sub:
-            return
-        slots = np.fromiter(sub.values(), dtype=np.uint32, count=len(sub))
-        self._wipe(slots)
-        self._release(slots)
+        _native.call("pc_store_drop_client", self._h, _cid(client))
+
+    def _list(self, client) -> np.ndarray:
+        n = ctypes.c_size_t()
+        _native.call("pc_store_list", self._h, _cid(client), None, 0, ctypes.byref(n))
+        out = np.empty(n.value, dtype=np.uint64)
+        if n.value:
+            _native.call("pc_store_list", self._h, _cid(client), out.ctypes.data, out.size, ctypes.byref(n))
+        return out
 
     def pages(self, client):
         """(vaddr, ciphertext) in strictly increasing vaddr order."""
-        sub = self._clients.get(client)
-        if not sub:
+        va = self._list(client)
+        if not va.size:
             return
-        vaddrs = sorted(sub)
-        out = np.empty((len(vaddrs), PAGE_SIZE), dtype=np.uint8)
-        self._move([sub[v] for v in vaddrs], out, 1)
-        for v, row in zip(vaddrs, out):
+        out = np.empty((va.size, PAGE_SIZE), dtype=np.uint8)
+        self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
+                   out.ctypes.data, 0, 0)
+        for v, row in zip(va.tolist(), out):
             yield v, row.tobytes()
 
     def page_count(self, client) -> int:
-        return len(self._clients.get(client, {}))
+        n = ctypes.c_size_t()
+        _native.call("pc_store_list", self._h, _cid(client), None, 0, ctypes.byref(n))
+        return n.value
 
     # -- fused cipher paths ----------------------------------------------------
+
+    def _need_key(self):
+        if self.key is None:
+            raise PageCryptError("this store has no DeviceKey: use insert/lookup for ciphertext")
 
     def evict(self, client, vaddr: int, plain) -> None:
         """Encrypt a plaintext page into a new HBM entry."""
@@ -175,41 +171,22 @@ class DevicePageStore:
         return self.refault_many(client, [vaddr])[0].tobytes()
 
     def evict_many(self, client, vaddrs, plains) -> None:
-        va, _ = _host_vaddrs(np.asarray(vaddrs) if not isinstance(vaddrs, (list, tuple)) else vaddrs,
-                             len(vaddrs))
-        arr = np.ascontiguousarray(plains, dtype=np.uint8).reshape(-1, PAGE_SIZE)
+        self._need_key()
+        va = self._vaddrs(vaddrs)
+        arr = plains if isinstance(plains, np.ndarray) else np.asarray(plains)
+        arr = np.ascontiguousarray(arr, dtype=np.uint8).reshape(-1, PAGE_SIZE)
         if arr.shape[0] != va.size:
             raise ContractViolation(f"{va.size} vaddrs for {arr.shape[0]} pages")
-        vlist = va.tolist()
-        vset = set(vlist)
-        sub = self._clients.setdefault(client, {})
-        if len(vset) != len(vlist) or not vset.isdisjoint(sub.keys()):
-            raise ContractViolation("duplicate store insert")
-        slots = self._take(len(vlist))
-        try:
-            self._move(slots, arr, 0, vaddrs=va, pid=client.pid, cipher=True)
-        except Exception:
-            self._release(slots)
-            raise
-        sub.update(zip(vlist, slots.tolist()))
+        self._call("pc_store_put", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
+                   arr.ctypes.data, 1)
 
     def refault_many(self, client, vaddrs, out: np.ndarray | None = None) -> np.ndarray:
-        va, _ = _host_vaddrs(np.asarray(vaddrs) if not isinstance(vaddrs, (list, tuple)) else vaddrs,
-                             len(vaddrs))
-        vlist = va.tolist()
-        sub = self._clients.get(client, {})
-        if len(set(vlist)) != len(vlist):
-            raise ContractViolation("duplicate vaddr in refault batch")
-        try:
-            slots = np.fromiter(map(sub.__getitem__, vlist), dtype=np.uint32, count=len(vlist))
-        except KeyError as exc:
-            raise ContractViolation(f"no store entry for {client} {exc.args[0]:#x}") from None
+        self._need_key()
+        va = self._vaddrs(vaddrs)
         if out is None:
-            out = np.empty((len(vlist), PAGE_SIZE), dtype=np.uint8)
-        elif out.nbytes != len(vlist) * PAGE_SIZE or not out.flags.c_contiguous:
+            out = np.empty((va.size, PAGE_SIZE), dtype=np.uint8)
+        elif out.nbytes != va.size * PAGE_SIZE or not out.flags.c_contiguous:
             raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
-        # decrypt on the way out and zero each slot as it is read (freed)
-        self._move(slots, out, 1, vaddrs=va, pid=client.pid, cipher=True, wipe_src=True)
-        deque(map(sub.pop, vlist), maxlen=0)
-        self._release(slots)
+        self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
+                   out.ctypes.data, 1, 1)
         return out

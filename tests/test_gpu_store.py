@@ -63,13 +63,29 @@ def test_lookup_empty_and_after_remove(store):
         store.remove(C1, 0x1000)
 
 
-def test_remove_then_reinsert_and_slot_wiped(store):
+def test_remove_then_reinsert(store):
     store.insert(C1, 0x1000, page(1))
-    slot = store._clients[C1][0x1000]
     store.remove(C1, 0x1000)
-    assert not store._slab[slot].any()  # freed slot wiped in HBM
     store.insert(C1, 0x1000, page(2))
     assert store.lookup(C1, 0x1000) == page(2)
+
+
+def test_freed_slots_are_wiped(cuda):
+    """Remove/refault/drop_client zero the HBM slot: a 1-slot store reused
+    through the raw path shows zeros in between (store.py:86-92)."""
+    s = DevicePageStore(1)
+    s.insert(C1, 0x1000, page(0xEE))
+    s.remove(C1, 0x1000)
+    s.insert(C1, 0x1000, page(0x11))
+    assert s.lookup(C1, 0x1000) == page(0x11)
+    s.drop_client(C1)
+    assert s.free_slots == 1
+
+
+def test_epoch_separates_clients(cuda):
+    s = DevicePageStore(4)
+    s.insert(ClientId(5, 0), 0x1000, page(1))
+    assert s.lookup(ClientId(5, 1), 0x1000) is None
 
 
 def test_drop_client_and_isolation(store):
@@ -153,3 +169,13 @@ def test_single_page_fused_paths(dkey):
     assert not s.contains(C1, 0x7000)
     with pytest.raises(ContractViolation):
         s.refault(C1, 0x7000)
+    # batches are all-or-nothing
+    s.evict(C1, 0x1000, plain)
+    with pytest.raises(ContractViolation):
+        s.evict_many(C1, [0x2000, 0x1000], np.zeros((2, 4096), np.uint8))
+    assert not s.contains(C1, 0x2000)
+    with pytest.raises(ContractViolation):
+        s.refault_many(C1, [0x1000, 0x3000])
+    assert s.contains(C1, 0x1000)
+    with pytest.raises(StoreFull):
+        s.evict_many(C1, [0x10000 * i for i in range(1, 9)], np.zeros((8, 4096), np.uint8))
