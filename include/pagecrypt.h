@@ -135,6 +135,14 @@ int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, i
  * the ticket done.  stop refuses with PC_ESTATE while requests are in flight
  * (WorkerPool.shutdown, workers.py:240-254). */
 typedef struct pc_service pc_service;
+/* Load every kernel of the library into the context now.  Under CUDA's
+ * default lazy module loading the first launch of any kernel waits for the
+ * context to go idle, i.e. forever while a persistent kernel runs; the
+ * service start calls this itself.  Other libraries' kernels (torch, ...)
+ * must be warmed before pc_service_start, or run with
+ * CUDA_MODULE_LOADING=EAGER, if they are first launched while the service
+ * is up. */
+int pc_preload(int device);
 int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int rounds, pc_service **out);
 int pc_service_submit(pc_service *svc, int worker, uint64_t vaddr, uint32_t pid, const void *src,
                       void *dst, uint64_t *ticket);
@@ -189,7 +197,12 @@ int pc_store_contains(pc_store *store, uint64_t client, uint64_t vaddr, int *fou
 int pc_store_list(pc_store *store, uint64_t client, uint64_t *vaddrs, size_t cap, size_t *n);
 int pc_store_free_slots(pc_store *store, size_t *n);
 
-/* ---- pinned host memory helpers --------------------------------------- */
+/* ---- pinned host memory helpers ---------------------------------------
+ * Note: freeing pinned memory (pc_host_free = cudaFreeHost) and
+ * pc_host_unregister synchronise the whole device and therefore block while
+ * a pc_service is running; the library itself recycles its own pinned
+ * buffers instead of freeing them and allocates device memory
+ * stream-ordered, so none of its entry points has that hazard. */
 int pc_host_alloc(size_t bytes, void **out);
 int pc_host_free(void *p);
 int pc_host_register(void *p, size_t bytes);

@@ -48,6 +48,7 @@ SIGNATURES = {
                                     c_void_p, c_void_p, c_size_t, c_int]),
     "pc_crypt_pages_multi": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_u64, c_u32,
                                      c_void_p, c_void_p, c_size_t, c_int]),
+    "pc_preload": (c_int, [c_int]),
     "pc_service_start": (c_int, [c_void_p, c_int, c_int, c_int, P(c_void_p)]),
     "pc_service_submit": (c_int, [c_void_p, c_int, c_u64, c_u32, c_void_p, c_void_p, P(c_u64)]),
     "pc_service_poll": (c_int, [c_void_p, c_int, c_u64, P(c_int)]),

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -316,6 +317,39 @@ bool pinned_alias(const void *p, void **dev) {
   return true;
 }
 
+// Process-wide recycler of pinned host buffers.  cudaFreeHost (like cudaFree
+// and cudaHostUnregister) synchronises the whole device, which never returns
+// while a persistent service kernel runs (tools/diag/persistent_probe), so the
+// library never frees pinned memory it allocated: released buffers are kept
+// by size and handed out again.  All are mapped + portable.
+struct PinnedPool {
+  std::mutex mu;
+  std::unordered_map<size_t, std::vector<void *>> free;
+};
+PinnedPool &pinned_pool() {
+  static PinnedPool *p = new PinnedPool(); // intentionally never destroyed
+  return *p;
+}
+cudaError_t pinned_get(void **out, size_t bytes) {
+  {
+    PinnedPool &pp = pinned_pool();
+    std::lock_guard<std::mutex> lk(pp.mu);
+    auto it = pp.free.find(bytes);
+    if (it != pp.free.end() && !it->second.empty()) {
+      *out = it->second.back();
+      it->second.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaHostAlloc(out, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+}
+void pinned_put(void *p, size_t bytes) {
+  if (!p) return;
+  PinnedPool &pp = pinned_pool();
+  std::lock_guard<std::mutex> lk(pp.mu);
+  pp.free[bytes].push_back(p);
+}
+
 // Per-device scratch for the synchronous seams and key staging (guarded): a
 // device buffer (stream-ordered allocation, so no call here ever forces a
 // device-wide synchronisation -- a persistent service kernel may be running)
@@ -343,7 +377,7 @@ int scratch_reserve(Scratch &sc, size_t need) {
   }
   if (sc.h) {
     wipe(sc.h, sc.cap);
-    CU(cudaFreeHost(sc.h));
+    pinned_put(sc.h, sc.cap);
   }
   sc.d = nullptr;
   sc.h = nullptr;
@@ -351,7 +385,7 @@ int scratch_reserve(Scratch &sc, size_t need) {
   const size_t cap = std::max<size_t>(need, 64 * 1024);
   CU(cudaMallocAsync(&sc.d, cap, sc.st));
   CU(cudaStreamSynchronize(sc.st));
-  CU(cudaHostAlloc(reinterpret_cast<void **>(&sc.h), cap, cudaHostAllocDefault));
+  CU(pinned_get(reinterpret_cast<void **>(&sc.h), cap));
   sc.cap = cap;
   return PC_OK;
 }
@@ -487,6 +521,8 @@ struct pc_engine {
   uint8_t *d_small = nullptr;
   size_t small_bytes = 0;
   std::unique_ptr<pc::HostPool> pool; // pageable <-> pinned bounce copies (lazy)
+  std::unique_ptr<pc::Runner> runner; // this engine's thread for multi-device calls (lazy)
+  std::mutex runner_mu;
 };
 
 // ===========================================================================
@@ -652,13 +688,13 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
     CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_vaddrs[s]), chunk_pages * 8, e->streams[0]));
     // d_pids: pids at [0, C), slab slots at [C, 2C); h_desc: vaddrs, pids, slots
     CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_pids[s]), chunk_pages * 8, e->streams[0]));
-    CUE(cudaHostAlloc(&e->h_desc[s], chunk_pages * 16, cudaHostAllocDefault));
+    CUE(pinned_get(reinterpret_cast<void **>(&e->h_desc[s]), chunk_pages * 16));
   }
-  CUE(cudaHostAlloc(&e->h_key, 256, cudaHostAllocDefault));
+  CUE(pinned_get(reinterpret_cast<void **>(&e->h_key), 256));
   CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_rawkey), 256, e->streams[0]));
   const size_t sm = tuning().small_max.load();
   e->small_bytes = 256 + sm * 16 + sm * PC_PAGE_SIZE;
-  CUE(cudaHostAlloc(&e->h_small, e->small_bytes, cudaHostAllocMapped));
+  CUE(pinned_get(reinterpret_cast<void **>(&e->h_small), e->small_bytes));
   CUE(cudaHostGetDevicePointer(reinterpret_cast<void **>(&e->hd_small), e->h_small, 0));
   CUE(cudaMallocAsync(reinterpret_cast<void **>(&e->d_small), e->small_bytes, e->streams[0]));
   CUE(cudaStreamSynchronize(e->streams[0]));
@@ -685,11 +721,11 @@ int pc_engine_destroy(pc_engine *e) {
     }
     cudaStreamSynchronize(s0);
   }
-  if (e->h_key) { wipe(e->h_key, 256); cudaFreeHost(e->h_key); }
-  if (e->h_small) { wipe(e->h_small, 256); cudaFreeHost(e->h_small); }
+  if (e->h_key) { wipe(e->h_key, 256); pinned_put(e->h_key, 256); }
+  if (e->h_small) { wipe(e->h_small, e->small_bytes); pinned_put(e->h_small, e->small_bytes); }
   for (size_t s = 0; s < e->streams.size(); ++s) {
-    if (e->h_bounce[s]) cudaFreeHost(e->h_bounce[s]);
-    if (e->h_desc[s]) cudaFreeHost(e->h_desc[s]);
+    if (e->h_bounce[s]) pinned_put(e->h_bounce[s], e->chunk_pages * PC_PAGE_SIZE);
+    if (e->h_desc[s]) pinned_put(e->h_desc[s], e->chunk_pages * 16);
     if (e->done[s]) cudaEventDestroy(e->done[s]);
     if (e->ev_h2d[s]) cudaEventDestroy(e->ev_h2d[s]);
     if (e->ev_k[s]) cudaEventDestroy(e->ev_k[s]);
@@ -779,7 +815,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   const bool dedicated = tuning().host_mode.load() == 2 && S >= 3;
   if (!pin_in || !pin_out) {
     for (int s = 0; s < S; ++s)
-      if (!e->h_bounce[s]) CU(cudaHostAlloc(&e->h_bounce[s], C * PC_PAGE_SIZE, cudaHostAllocDefault));
+      if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
     if (!e->pool) {
       const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
       e->pool.reset(new pc::HostPool(std::min(7u, hw > 1 ? hw / 2 : 0u)));
@@ -961,7 +997,7 @@ extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, siz
   const size_t C = e->chunk_pages;
   if (!pinned) {
     for (int s = 0; s < S; ++s)
-      if (!e->h_bounce[s]) CU(cudaHostAlloc(&e->h_bounce[s], C * PC_PAGE_SIZE, cudaHostAllocDefault));
+      if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
     if (!e->pool) {
       const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
       e->pool.reset(new pc::HostPool(std::min(7u, hw > 1 ? hw / 2 : 0u)));
@@ -1066,27 +1102,93 @@ int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, i
                          const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0, uint32_t pid0,
                          const void *in, void *out, size_t n, int rounds) {
   if (!engines || !keys || n_dev <= 0) return fail(PC_EINVAL, "need >= 1 engine and key");
+  for (int g = 0; g < n_dev; ++g)
+    if (!engines[g] || engines[g]->magic != kEngineMagic) return fail(PC_ESTATE, "engine %d is not live", g);
   std::vector<int> rcs(n_dev, PC_OK);
   std::vector<std::string> errs(n_dev);
-  std::vector<std::thread> th;
-  for (int g = 0; g < n_dev; ++g) {
-    th.emplace_back([&, g] {
-      const size_t lo = n * g / n_dev, hi = n * (g + 1) / n_dev;
-      if (hi == lo) return;
-      rcs[g] = pc_crypt_pages_host(engines[g], keys[g], nullptr, vaddrs ? vaddrs + lo : nullptr,
-                                   pids ? pids + lo : nullptr, vaddr0 + 4096ull * lo, pid0,
-                                   static_cast<const uint8_t *>(in) + lo * PC_PAGE_SIZE,
-                                   static_cast<uint8_t *>(out) + lo * PC_PAGE_SIZE, hi - lo, rounds);
-      if (rcs[g] != PC_OK) errs[g] = pc_last_error();
-    });
+  auto job = [&](int g) {
+    const size_t lo = n * g / n_dev, hi = n * (g + 1) / n_dev;
+    if (hi == lo) return;
+    rcs[g] = pc_crypt_pages_host(engines[g], keys[g], nullptr, vaddrs ? vaddrs + lo : nullptr,
+                                 pids ? pids + lo : nullptr, vaddr0 + 4096ull * lo, pid0,
+                                 static_cast<const uint8_t *>(in) + lo * PC_PAGE_SIZE,
+                                 static_cast<uint8_t *>(out) + lo * PC_PAGE_SIZE, hi - lo, rounds);
+    if (rcs[g] != PC_OK) errs[g] = pc_last_error();
+  };
+  // engines 1..G-1 run on their persistent runner threads, engine 0 here
+  std::vector<std::function<void()>> waits;
+  for (int g = 1; g < n_dev; ++g) {
+    pc_engine *e = engines[g];
+    {
+      std::lock_guard<std::mutex> lk(e->runner_mu);
+      if (!e->runner) e->runner.reset(new pc::Runner());
+    }
+    waits.push_back(e->runner->submit([&job, g] { job(g); }));
   }
-  for (auto &t : th) t.join();
+  job(0);
+  for (auto &w : waits) w();
   for (int g = 0; g < n_dev; ++g)
     if (rcs[g] != PC_OK) return fail(rcs[g], "device slot %d: %s", g, errs[g].c_str());
   return PC_OK;
 }
 
 } // extern "C"
+
+// ---- module preloading ------------------------------------------------------------
+// With CUDA's default lazy module loading, the first launch of a kernel loads
+// it into the context, and that load waits for the context to go idle -- it
+// deadlocks behind a persistent kernel (measured: tools/diag/persistent_probe).
+// pc_preload loads every kernel of this library up front; pc_service_start
+// calls it before launching the service.
+namespace {
+template <typename F>
+cudaError_t touch(F *fn) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, fn);
+}
+
+template <int R>
+cudaError_t touch_rounds() {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+  for (uint32_t m : kRotMasks) (void)m;
+  acc(touch(pc::k_crypt_blocks<R, 0x00000000u>));
+  acc(touch(pc::k_crypt_blocks<R, 0x88888888u>));
+  acc(touch(pc::k_crypt_blocks<R, 0x888888AAu>));
+  acc(touch(pc::k_crypt_blocks<R, 0x88888AAAu>));
+  acc(touch(pc::k_crypt_blocks<R, 0xAAAA8888u>));
+  acc(touch(pc::k_crypt_blocks<R, 0xAAAAAAAAu>));
+  acc(touch(pc::k_crypt_pages<R>));
+  acc(touch(pc::k_crypt_pages_coalesced<R>));
+  acc(touch(pc::k_crypt_pages_tma<R, kTmaStages>));
+  acc(touch(pc::k_crypt_pages_async<R, true>));
+  acc(touch(pc::k_crypt_pages_async<R, false>));
+  acc(touch(pc::k_keystream_seeds<R>));
+  acc(touch(pc::k_service<R>));
+  acc(touch(pc::k_slab_move<R, 0>));
+  acc(touch(pc::k_slab_move<R, 1>));
+  return e;
+}
+} // namespace
+
+extern "C" int pc_preload(int device) {
+  DeviceGuard g(device);
+  CU(g.err);
+  CU(touch_rounds<8>());
+  CU(touch_rounds<12>());
+  CU(touch_rounds<20>());
+  CU(touch(pc::k_keygen));
+  CU(touch(pc::k_slab_wipe));
+  CU(touch(pc::k_intpeak<0>));
+  CU(touch(pc::k_intpeak<1>));
+  CU(touch(pc::k_intpeak<2>));
+  CU(touch(pc::k_intpeak<3>));
+  CU(touch(pc::k_intpeak<4>));
+  CU(touch(pc::k_intpeak<5>));
+  CU(touch(pc::k_intpeak<6>));
+  CU(touch(pc::k_intpeak<7>));
+  return PC_OK;
+}
 
 // ---- (vii) persistent crypto-worker service -------------------------------------
 namespace {
@@ -1166,6 +1268,8 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     return fail(PC_EINVAL, "n_workers must be 1..%d (all workers must be co-resident), got %d", maxw, n_workers);
   DeviceGuard g(key->device);
   CU(g.err);
+  rc = pc_preload(key->device); // nothing of ours may lazy-load behind the service
+  if (rc != PC_OK) return rc;
   auto *s = new pc_service();
   s->device = key->device;
   s->n_workers = n_workers;
@@ -1187,10 +1291,11 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
       cudaFreeAsync(s->dev, s->st);
       cudaStreamSynchronize(s->st);
     }
-    if (s->h_slots) cudaFreeHost(s->h_slots);
-    if (s->h_pages) cudaFreeHost(s->h_pages);
-    if (s->h_ctrl) cudaFreeHost(s->h_ctrl);
-    if (s->h_bell) cudaFreeHost(s->h_bell);
+    const size_t ns = static_cast<size_t>(s->n_workers) * s->ring;
+    pinned_put(s->h_slots, ns * sizeof(pc::SvcSlot));
+    pinned_put(s->h_pages, ns * PC_PAGE_SIZE);
+    pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
+    pinned_put(s->h_bell, s->n_workers * sizeof(uint64_t));
     if (s->st) cudaStreamDestroy(s->st);
     delete s;
     return code;
@@ -1201,17 +1306,17 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     if (e_ != cudaSuccess) return bail(fail(PC_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); \
   } while (0)
   CUS(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
-  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_slots), nslots * sizeof(pc::SvcSlot), cudaHostAllocMapped));
-  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_pages), nslots * PC_PAGE_SIZE, cudaHostAllocMapped));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_slots), nslots * sizeof(pc::SvcSlot)));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_pages), nslots * PC_PAGE_SIZE));
   const size_t ctrl_bytes = (64 + static_cast<size_t>(n_workers)) * 4;
-  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_ctrl), ctrl_bytes, cudaHostAllocMapped));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_ctrl), ctrl_bytes));
   std::memset(s->h_slots, 0, nslots * sizeof(pc::SvcSlot));
   std::memset(s->h_pages, 0, nslots * PC_PAGE_SIZE);
   std::memset(s->h_ctrl, 0, ctrl_bytes);
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_slots), s->h_slots, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_pages), s->h_pages, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_ctrl), s->h_ctrl, 0));
-  CUS(cudaHostAlloc(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(uint64_t), cudaHostAllocMapped));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(uint64_t)));
   std::memset(s->h_bell, 0, n_workers * sizeof(uint64_t));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_bell), s->h_bell, 0));
   CUS(cudaMallocAsync(reinterpret_cast<void **>(&s->dev), sizeof(pc::SvcDev), s->st));
@@ -1380,10 +1485,10 @@ int pc_service_stop(pc_service *s) {
   wipe(s->h_pages, nslots * PC_PAGE_SIZE);
   cudaFreeAsync(s->dev, s->st);
   cudaStreamSynchronize(s->st);
-  cudaFreeHost(s->h_slots);
-  cudaFreeHost(s->h_pages);
-  cudaFreeHost(s->h_ctrl);
-  cudaFreeHost(s->h_bell);
+  pinned_put(s->h_slots, nslots * sizeof(pc::SvcSlot));
+  pinned_put(s->h_pages, nslots * PC_PAGE_SIZE);
+  pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
+  pinned_put(s->h_bell, s->n_workers * sizeof(uint64_t));
   cudaStreamDestroy(s->st);
   s->magic = 0;
   delete s;
