@@ -347,6 +347,7 @@ def main() -> None:
             extras["latency_host_small"] = latency_sweep(pc, key, local_rank)
             extras["latency_service_1page"] = service_latency(local_rank)
             extras["hbm_store"] = store_throughput(pc, key, local_rank)
+            extras["pager"] = pager_rate(pc, key, local_rank)
     del host_in, host_out
 
     cpu = None
@@ -440,6 +441,48 @@ def store_throughput(pc, key, device: int, n: int = 65536) -> dict:
     return {"pages": n, "evict_gbs": round(n * PAGE / (t1 - t0) / 1e9, 2),
             "refault_gbs": round(n * PAGE / (t2 - t1) / 1e9, 2), "roundtrip_identical": ok,
             "note": "one batch each way, pinned host buffers, includes the Python index updates"}
+
+
+def pager_rate(pc, key, device: int) -> dict:
+    """faults/s through WindowPager (window 64) with one
+    fault per call (the reference's flow) and with 64-fault batches."""
+    from paper_2004_09252_b200.pager import WindowPager
+    from paper_2004_09252_b200.store import DevicePageStore
+    from paper_2004_09252_b200.workers import ClientId
+
+    res = {}
+    pages = [BASE_VADDR + PAGE * i for i in range(4096)]
+    for batch in (1, 64):
+        st = DevicePageStore(8192, key, device=device)
+        mem = {}
+
+        def fetch(c, vs):
+            return np.stack([mem.pop(v) for v in vs])
+
+        pg = WindowPager(st, fetch, window_capacity=64)
+        c = ClientId(1, 0)
+        pg.register(c)
+        n = 0
+        t0 = time.perf_counter()
+        for rep in range(2):  # second pass refaults every page
+            for i in range(0, len(pages), batch):
+                vs = pages[i:i + batch]
+                out = pg.fault_batch(c, vs)
+                for v, row in zip(vs, out):
+                    if pg._window(c).resident(v):
+                        mem[v] = row
+                n += len(vs)
+            for v in pg.window(c):  # drain the window between passes
+                pass
+            t_mid = time.perf_counter()
+            if rep == 0:
+                pg.unregister(c)
+                pg.register(c)
+                mem.clear()
+        el = time.perf_counter() - t0
+        res[f"batch{batch}"] = {"faults_per_s": round(n / el), "gbs": round(n * PAGE / el / 1e9, 3)}
+        st.close()
+    return res
 
 
 def service_latency(device: int, reps: int = 2000) -> dict:

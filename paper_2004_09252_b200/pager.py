@@ -1,0 +1,173 @@
+"""Batched fault/eviction resolution over the HBM page store.
+
+The reference resolves one fault at a time (``Orchestrator.handle_fault`` /
+``evict_page``, ``pkg/src/pagecrypt/orchestrator.py:175-240``): look the page
+up in the store, decrypt it (or hand out a zero page on first touch), admit
+it into the client's FIFO sliding window (``window.py:31-45``) and, when the
+window overflows, pull the oldest resident page back from the client,
+encrypt it and store it -- two synchronous single-page crypto calls per
+fault.  ``WindowPager`` keeps those semantics and adds ``fault_batch``: all
+faults of a batch are resolved with ONE ``refault_many`` (decrypt out of
+HBM) and ONE ``evict_many`` (encrypt into HBM), so the GPU sees real batches.
+
+A batch is equivalent to faulting its pages one by one in order (checked in
+``tests/test_gpu_pager.py``): a page evicted by a later fault of the same
+batch is stored with the plaintext it was just resolved to, which is what
+the client would hand back.
+
+The transport to the client (``transport.py``, ``client.py``) is out of
+scope; the caller supplies ``fetch_evicted(client, vaddrs) -> uint8[m, 4096]``,
+the data-port pull of ``client.py:251-265``.
+"""
+
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ContractViolation
+from .store import DevicePageStore
+
+PAGE_SIZE = 4096
+
+
+class SlidingWindow:
+    """Bounded FIFO of plaintext-resident vaddrs (window.py:15-67)."""
+
+    MAX_CAPACITY = 4096
+
+    def __init__(self, capacity: int = 16):
+        if not 1 <= capacity <= self.MAX_CAPACITY:
+            raise ContractViolation(f"window capacity {capacity} outside 1..{self.MAX_CAPACITY}")
+        self.capacity = capacity
+        self._queue: deque[int] = deque()
+        self._members: set[int] = set()
+
+    def admit(self, vaddr: int):
+        if vaddr in self._members:
+            raise ContractViolation(f"page {vaddr:#x} already in window")
+        evicted = None
+        if len(self._queue) == self.capacity:
+            evicted = self._queue.popleft()
+            self._members.discard(evicted)
+        self._queue.append(vaddr)
+        self._members.add(vaddr)
+        return evicted
+
+    def remove(self, vaddr: int) -> bool:
+        if vaddr not in self._members:
+            return False
+        self._members.discard(vaddr)
+        self._queue.remove(vaddr)
+        return True
+
+    def resident(self, vaddr: int) -> bool:
+        return vaddr in self._members
+
+    def __len__(self) -> int:
+        return len(self._queue)
+
+    def members(self) -> list[int]:
+        return list(self._queue)
+
+
+@dataclass
+class PagerMetrics:
+    """Per-client counters (orchestrator.py:41-63)."""
+
+    faults: int = 0
+    first_touch_faults: int = 0
+    evictions: int = 0
+    encrypt_ops: int = 0
+    decrypt_ops: int = 0
+    gpu_batches: int = 0
+
+
+class WindowPager:
+    def __init__(self, store: DevicePageStore, fetch_evicted, window_capacity: int = 16):
+        if store.key is None:
+            raise ContractViolation("the pager needs a store with a DeviceKey")
+        SlidingWindow(window_capacity)  # validate range up front
+        self.store = store
+        self.fetch_evicted = fetch_evicted
+        self.window_capacity = window_capacity
+        self._windows: dict[object, SlidingWindow] = {}
+        self.metrics: dict[object, PagerMetrics] = {}
+
+    def register(self, client) -> None:
+        if client in self._windows:
+            raise ContractViolation(f"client {client} already registered")
+        self._windows[client] = SlidingWindow(self.window_capacity)
+        self.metrics[client] = PagerMetrics()
+
+    def unregister(self, client) -> None:
+        """Drop all server-side state of a client; its ciphertext is wiped."""
+        if self._windows.pop(client, None) is not None:
+            self.store.drop_client(client)
+
+    def window(self, client) -> list[int]:
+        return self._window(client).members()
+
+    def _window(self, client) -> SlidingWindow:
+        w = self._windows.get(client)
+        if w is None:
+            raise ContractViolation(f"unknown client {client}")
+        return w
+
+    def fault(self, client, vaddr: int) -> bytes:
+        """Resolve one fault (handle_fault, orchestrator.py:175-211)."""
+        return self.fault_batch(client, [vaddr])[0].tobytes()
+
+    def fault_batch(self, client, vaddrs) -> np.ndarray:
+        """Resolve faults on distinct, non-resident pages, in order; returns
+        their plaintexts as uint8[k, 4096]."""
+        win = self._window(client)
+        m = self.metrics[client]
+        vlist = [int(v) for v in vaddrs]
+        if len(set(vlist)) != len(vlist):
+            raise ContractViolation("a batch faults each page once")
+        for v in vlist:
+            if v % PAGE_SIZE:
+                raise ContractViolation(f"vaddr {v:#x} not page-aligned")
+            if win.resident(v):
+                raise ContractViolation(f"fault on resident page {v:#x}")
+        k = len(vlist)
+        out = np.zeros((k, PAGE_SIZE), dtype=np.uint8)  # first touch: zero pages
+        if not k:
+            return out
+        # 1. refaults: one decrypt-out-of-HBM batch (entries are removed)
+        refault_idx = [i for i, v in enumerate(vlist) if self.store.contains(client, v)]
+        if refault_idx:
+            plains = self.store.refault_many(client, [vlist[i] for i in refault_idx])
+            out[refault_idx] = plains
+            m.decrypt_ops += len(refault_idx)
+            m.gpu_batches += 1
+        m.first_touch_faults += k - len(refault_idx)
+        m.faults += k
+        # 2. window admission in fault order; collect evictions
+        batch_pos = {v: i for i, v in enumerate(vlist)}
+        evicted: list[int] = []
+        for v in vlist:
+            e = win.admit(v)
+            if e is not None:
+                evicted.append(e)
+        if not evicted:
+            return out
+        # 3. evictions: pages resident before the batch come back from the
+        #    client; pages faulted in by this batch carry their resolved bytes
+        from_client = [e for e in evicted if e not in batch_pos]
+        plain_ev = np.empty((len(evicted), PAGE_SIZE), dtype=np.uint8)
+        if from_client:
+            got = np.ascontiguousarray(self.fetch_evicted(client, from_client), dtype=np.uint8)
+            got = got.reshape(len(from_client), PAGE_SIZE)
+            row = {e: j for j, e in enumerate(from_client)}
+        for j, e in enumerate(evicted):
+            plain_ev[j] = out[batch_pos[e]] if e in batch_pos else got[row[e]]
+        self.store.evict_many(client, evicted, plain_ev)
+        plain_ev.fill(0)  # scratch_evict.wipe(), orchestrator.py:239
+        m.evictions += len(evicted)
+        m.encrypt_ops += len(evicted)
+        m.gpu_batches += 1
+        return out
