@@ -445,7 +445,9 @@ def store_throughput(pc, key, device: int, n: int = 65536) -> dict:
 
 def pager_rate(pc, key, device: int) -> dict:
     """faults/s through WindowPager (window 64) with one
-    fault per call (the reference's flow) and with 64-fault batches."""
+    fault per call (the reference's flow) and with 64-fault batches.  Two
+    passes over 4096 pages: first touches + evictions, then refaults +
+    evictions."""
     from paper_2004_09252_b200.pager import WindowPager
     from paper_2004_09252_b200.store import DevicePageStore
     from paper_2004_09252_b200.workers import ClientId
@@ -455,32 +457,26 @@ def pager_rate(pc, key, device: int) -> dict:
     for batch in (1, 64):
         st = DevicePageStore(8192, key, device=device)
         mem = {}
-
-        def fetch(c, vs):
-            return np.stack([mem.pop(v) for v in vs])
-
-        pg = WindowPager(st, fetch, window_capacity=64)
+        pg = WindowPager(st, lambda c, vs: np.stack([mem.pop(v) for v in vs]), window_capacity=64)
         c = ClientId(1, 0)
         pg.register(c)
         n = 0
         t0 = time.perf_counter()
-        for rep in range(2):  # second pass refaults every page
+        for _ in range(2):
             for i in range(0, len(pages), batch):
-                vs = pages[i:i + batch]
+                vs = [v for v in pages[i:i + batch] if v not in mem]
+                if not vs:
+                    continue
                 out = pg.fault_batch(c, vs)
                 for v, row in zip(vs, out):
-                    if pg._window(c).resident(v):
+                    if v in pg._window(c)._members:
                         mem[v] = row
                 n += len(vs)
-            for v in pg.window(c):  # drain the window between passes
-                pass
-            t_mid = time.perf_counter()
-            if rep == 0:
-                pg.unregister(c)
-                pg.register(c)
-                mem.clear()
         el = time.perf_counter() - t0
-        res[f"batch{batch}"] = {"faults_per_s": round(n / el), "gbs": round(n * PAGE / el / 1e9, 3)}
+        m = pg.metrics[c]
+        res[f"batch{batch}"] = {"faults_per_s": round(n / el), "gbs": round(n * PAGE / el / 1e9, 3),
+                                "decrypts": m.decrypt_ops, "encrypts": m.encrypt_ops, "gpu_batches": m.gpu_batches}
+        pg.unregister(c)
         st.close()
     return res
 

@@ -991,6 +991,31 @@ extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, siz
   std::lock_guard<std::mutex> lk(e->mu);
   DeviceGuard g(e->device);
   CU(g.err);
+  if (n <= std::min<size_t>(64, tuning().small_max.load())) {
+    // small batch (a fault's refault/evict): one zero-copy launch over the
+    // engine's mapped staging -- slots, vaddrs and pages read/written by the
+    // kernel across PCIe, no DMA round trips
+    uint8_t *h = e->h_small;
+    uint8_t *hd = e->hd_small;
+    std::memcpy(h, slots, n * 4);
+    if (key && vaddrs) std::memcpy(h + 256, vaddrs, n * 8);
+    if (dir == 0) std::memcpy(h + 1024, host, n * PC_PAGE_SIZE);
+    const pc::PageDesc d{key && vaddrs ? reinterpret_cast<const uint64_t *>(hd + 256) : nullptr, nullptr, vaddr0, pid0};
+    const uint32_t *k = key ? key->d_words : nullptr;
+    cudaStream_t st = e->streams[0];
+    switch (rounds) {
+      case 8: launch_slab_r<8>(dir, k, d, reinterpret_cast<const uint32_t *>(hd), slab, hd + 1024, n, wipe_src, st); break;
+      case 12: launch_slab_r<12>(dir, k, d, reinterpret_cast<const uint32_t *>(hd), slab, hd + 1024, n, wipe_src, st); break;
+      default: launch_slab_r<20>(dir, k, d, reinterpret_cast<const uint32_t *>(hd), slab, hd + 1024, n, wipe_src, st); break;
+    }
+    cudaError_t err = cudaGetLastError();
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (err == cudaSuccess) err = e2;
+    if (err == cudaSuccess && dir == 1) std::memcpy(host, h + 1024, n * PC_PAGE_SIZE);
+    wipe(h + 1024, n * PC_PAGE_SIZE); // plaintext passed through the staging
+    CU(err);
+    return PC_OK;
+  }
   void *host_dev = nullptr;
   const bool pinned = pinned_alias(host, &host_dev);
   const int S = e->n_streams;
