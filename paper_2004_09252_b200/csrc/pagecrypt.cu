@@ -7,6 +7,7 @@
 // (pkg/src/pagecrypt/workers.py: key slots :168,174-202,240-254; routing
 // :204-206 -> the page-range partitioner pc_crypt_pages_multi).
 #include <cuda_runtime.h>
+#include <immintrin.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -1220,14 +1221,14 @@ namespace {
 constexpr uint32_t kServiceMagic = 0x73766331u; // "svc1"
 
 int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key, pc::SvcSlot *slots,
-                   uint4 *pages, uint32_t ring, const uint64_t *bell, const uint32_t *stop, uint32_t *started,
-                   pc::SvcDev *dev) {
+                   uint4 *pages, uint32_t ring, const pc::SvcBell *bell, const uint32_t *stop, uint32_t *started,
+                   pc::SvcDev *dev, uint4 *hdr) {
   const unsigned grid = static_cast<unsigned>(workers) + 1; // + the dispatcher
   const uint32_t nw = static_cast<uint32_t>(workers);
   switch (rounds) {
-    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev); break;
-    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev); break;
-    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev); break;
+    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr); break;
+    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr); break;
+    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr); break;
   }
   CU(cudaGetLastError());
   return PC_OK;
@@ -1250,8 +1251,9 @@ struct pc_service {
   pc::SvcSlot *h_slots = nullptr, *d_slots = nullptr; // mapped pinned
   uint8_t *h_pages = nullptr, *d_pages = nullptr;     // mapped pinned
   uint32_t *h_ctrl = nullptr, *d_ctrl = nullptr;      // [0] stop, [64..] started[w]
-  uint64_t *h_bell = nullptr, *d_bell = nullptr;      // per worker: tickets published (in order)
+  pc::SvcBell *h_bell = nullptr, *d_bell = nullptr;   // per worker: tickets published (in order) + header
   pc::SvcDev *dev = nullptr;                          // device-memory doorbell mirror
+  uint4 *hdr = nullptr;                               // forwarded headers, n_workers x ring
   // Host-side slot protocol.  Slot j of a worker carries tickets j, j+R, ...
   //   next[j]  = the ticket whose result is the next to be delivered in slot j
   //   claim[j] = ticket a finisher may claim (CAS t -> t+R) to deliver it
@@ -1312,15 +1314,14 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     s->dst[i] = nullptr;
   }
   auto bail = [&](int code) {
-    if (s->dev) {
-      cudaFreeAsync(s->dev, s->st);
-      cudaStreamSynchronize(s->st);
-    }
+    if (s->dev) cudaFreeAsync(s->dev, s->st);
+    if (s->hdr) cudaFreeAsync(s->hdr, s->st);
+    if (s->dev || s->hdr) cudaStreamSynchronize(s->st);
     const size_t ns = static_cast<size_t>(s->n_workers) * s->ring;
     pinned_put(s->h_slots, ns * sizeof(pc::SvcSlot));
     pinned_put(s->h_pages, ns * PC_PAGE_SIZE);
     pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
-    pinned_put(s->h_bell, s->n_workers * sizeof(uint64_t));
+    pinned_put(s->h_bell, s->n_workers * sizeof(pc::SvcBell));
     if (s->st) cudaStreamDestroy(s->st);
     delete s;
     return code;
@@ -1341,16 +1342,18 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_slots), s->h_slots, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_pages), s->h_pages, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_ctrl), s->h_ctrl, 0));
-  CUS(pinned_get(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(uint64_t)));
-  std::memset(s->h_bell, 0, n_workers * sizeof(uint64_t));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(pc::SvcBell)));
+  std::memset(s->h_bell, 0, n_workers * sizeof(pc::SvcBell));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_bell), s->h_bell, 0));
   CUS(cudaMallocAsync(reinterpret_cast<void **>(&s->dev), sizeof(pc::SvcDev), s->st));
   CUS(cudaMemsetAsync(s->dev, 0, sizeof(pc::SvcDev), s->st));
+  CUS(cudaMallocAsync(reinterpret_cast<void **>(&s->hdr), nslots * sizeof(uint4), s->st));
+  CUS(cudaMemsetAsync(s->hdr, 0xff, nslots * sizeof(uint4), s->st)); // tags match no ticket
   CUS(cudaStreamSynchronize(s->st));
 #undef CUS
   // the kernel reads the key once; it must be resident before we report success
   rc = service_launch(rounds, n_workers, s->st, key->d_words, s->d_slots, reinterpret_cast<uint4 *>(s->d_pages),
-                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev);
+                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev, s->hdr);
   if (rc != PC_OK) return bail(rc);
   const auto t0 = std::chrono::steady_clock::now();
   volatile uint32_t *started = s->h_ctrl + 64;
@@ -1432,14 +1435,23 @@ int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, c
   sl->vaddr = vaddr;
   sl->pid = pid;
   std::atomic_thread_fence(std::memory_order_release);
-  // publish in ticket order: the doorbell counts consecutive published tickets
-  auto *bell = reinterpret_cast<std::atomic<uint64_t> *>(s->h_bell + worker);
+  // publish in ticket order: the doorbell counts consecutive published
+  // tickets; the header of the newest one rides along (dispatcher fast path)
+  pc::SvcBell *hb = s->h_bell + worker;
+  auto *count = reinterpret_cast<std::atomic<uint32_t> *>(&hb->count);
   uint32_t bspins = 0;
-  while (bell->load(std::memory_order_acquire) != t) {
+  while (count->load(std::memory_order_acquire) != static_cast<uint32_t>(t)) {
     if (++bspins > 64) std::this_thread::yield();
     else cpu_relax();
   }
-  bell->store(t + 1, std::memory_order_release);
+  // count, pid and vaddr in ONE aligned 16-byte store (atomic on x86-64
+  // CPUs with AVX), so the dispatcher's 16-byte read never sees a count
+  // paired with another ticket's header
+  std::atomic_thread_fence(std::memory_order_release);
+  const __m128i v = _mm_set_epi64x(static_cast<long long>(vaddr),
+                                   static_cast<long long>((static_cast<uint64_t>(pid) << 32) |
+                                                          static_cast<uint32_t>(t + 1)));
+  _mm_store_si128(reinterpret_cast<__m128i *>(hb), v);
   *ticket = t;
   return PC_OK;
 }
@@ -1509,11 +1521,12 @@ int pc_service_stop(pc_service *s) {
   const size_t nslots = static_cast<size_t>(s->n_workers) * s->ring;
   wipe(s->h_pages, nslots * PC_PAGE_SIZE);
   cudaFreeAsync(s->dev, s->st);
+  cudaFreeAsync(s->hdr, s->st);
   cudaStreamSynchronize(s->st);
   pinned_put(s->h_slots, nslots * sizeof(pc::SvcSlot));
   pinned_put(s->h_pages, nslots * PC_PAGE_SIZE);
   pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
-  pinned_put(s->h_bell, s->n_workers * sizeof(uint64_t));
+  pinned_put(s->h_bell, s->n_workers * sizeof(pc::SvcBell));
   cudaStreamDestroy(s->st);
   s->magic = 0;
   delete s;

@@ -12,12 +12,14 @@
 // Here: one 32-thread CTA per worker plus one dispatcher CTA.  Each worker
 // owns a ring of C slots in mapped pinned host memory: a 64-byte header
 // (vaddr, pid, done_seq) and a 4 KiB page.  Request t of a worker lives in
-// slot t % C.  Producers publish tickets in order per worker by advancing
-// doorbell[w] (mapped host memory).  Only the dispatcher polls the doorbells
-// over PCIe -- one coalesced read for all workers per poll -- and forwards
-// them into device memory, where the idle workers poll cheaply (L2).  A worker
-// that sees bell > head reads the slot header and the page in one PCIe round
-// trip, XORs the page in place and stores done_seq = t+1.  The key is loaded
+// slot t % C.  Producers publish tickets in order per worker by storing
+// doorbell[w] = {count, pid, vaddr of the newest ticket} with one 16-byte
+// store (mapped host memory).  Only the dispatcher polls the doorbells over
+// PCIe -- one coalesced read for all workers per poll -- and forwards them
+// into device memory, where the idle workers poll cheaply (L2).  A worker
+// whose next ticket is the newest one gets its header with the bell and
+// computes the keystream while the page bytes cross PCIe; otherwise it reads
+// the slot header.  It XORs the page in place and stores done_seq = t+1.  The key is loaded
 // into registers once at start (the device copy can then be destroyed); the
 // cipher state never leaves registers (ptxas: 0 bytes stack/spill).
 #pragma once
@@ -84,8 +86,26 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t *p, uint32_t v) {
 __device__ __forceinline__ uint32_t svc_swz(uint32_t q) { return (q & ~7u) | ((q ^ (q >> 3)) & 7u); }
 
 // Device-side control block (device memory).
+// Host doorbell of one worker (mapped pinned memory, 16 bytes, written by
+// the producer that publishes ticket t: vaddr and pid of t first, then
+// count = t + 1), so one 16-byte read gives the dispatcher the count AND the
+// header of the latest ticket.
+struct alignas(16) SvcBell {
+  uint32_t count; // tickets published, mod 2^32
+  uint32_t pid;   // of the latest published ticket
+  uint64_t vaddr;
+};
+static_assert(sizeof(SvcBell) == 16, "one 16-byte read per doorbell");
+
+// Device-memory mirror of the doorbells.  bell[w] is the 64-bit count of
+// published tickets.  When the dispatcher forwards a new count it also files
+// the header of the newest ticket T under hdr[w * ring + T % ring] =
+// {vaddr_lo, vaddr_hi, pid, tag = T} BEFORE releasing the count, so the
+// entry for a ticket is never rewritten while that ticket is pending (the
+// ring's back-pressure), and a worker that finds tag == its ticket uses it;
+// any other tag means the header was never forwarded -> read the slot.
 struct SvcDev {
-  uint64_t bell[4096]; // forwarded doorbells, one per worker
+  uint64_t bell[4096];
   uint32_t stop;
 };
 
@@ -98,7 +118,8 @@ __device__ __forceinline__ void named_bar(uint32_t count) {
 template <int ROUNDS>
 __global__ void __launch_bounds__(64, 1)
 k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32_t ring, uint32_t n_workers,
-          const uint64_t *host_bell, const uint32_t *host_stop, uint32_t *started, SvcDev *dev) {
+          const SvcBell *host_bell, const uint32_t *host_stop, uint32_t *started, SvcDev *dev,
+          uint4 *hdr) {
   __shared__ uint4 tile[256]; // one 4 KiB page
   const uint32_t lane = threadIdx.x;
   if (blockIdx.x == n_workers) {
@@ -109,26 +130,38 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
     constexpr uint32_t kMaxPerLane = 4096 / 32;
     uint32_t idle = 0;
     for (;;) {
-      uint64_t b[4];
+      // one PCIe round trip per poll for up to 256 workers: all bells and the
+      // stop flag are loaded together, then one acquire fence
+      uint4 b[8];
       bool moved = false;
-      for (uint32_t w0 = 0; w0 < n_workers; w0 += 128) {
+      bool stop = false;
+      for (uint32_t w0 = 0; w0 < n_workers; w0 += 256) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           const uint32_t w = w0 + u * 32 + lane;
-          b[u] = w < n_workers ? ld_relaxed_sys(host_bell + w) : 0;
+          b[u] = w < n_workers ? ld_volatile_v4(reinterpret_cast<const uint4 *>(host_bell + w))
+                               : make_uint4(0, 0, 0, 0);
         }
+        if (w0 == 0) stop = ld_volatile_u32(host_stop) != 0u;
         asm volatile("fence.acq_rel.sys;" ::: "memory");
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           const uint32_t w = w0 + u * 32 + lane;
-          if (w < n_workers && b[u] != dev->bell[w]) {
-            st_release_gpu(&dev->bell[w], b[u]);
+          if (w >= n_workers) continue;
+          const uint64_t cur = dev->bell[w];
+          const uint32_t delta = b[u].x - static_cast<uint32_t>(cur);
+          if (delta != 0) {
+            const uint64_t cnt = cur + delta;
+            const uint64_t newest = cnt - 1;
+            st_volatile_v4(&hdr[static_cast<uint64_t>(w) * ring + newest % ring],
+                           make_uint4(b[u].z, b[u].w, b[u].y, static_cast<uint32_t>(newest)));
+            __threadfence();                 // header filed before the count
+            st_release_gpu(&dev->bell[w], cnt);
             moved = true;
           }
         }
       }
       (void)kMaxPerLane;
-      const bool stop = ld_volatile_u32(host_stop) != 0u;
       if (__any_sync(0xffffffffu, stop)) {
         if (lane == 0) atomicExch(&dev->stop, 1u);
         break;
@@ -158,11 +191,10 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
   }
   SvcSlot *myring = slots + static_cast<uint64_t>(worker) * ring;
   uint4 *mypages = pages + static_cast<uint64_t>(worker) * ring * 256;
-  uint64_t bell = 0;
-
   for (uint64_t head = 0;; ++head) {
     // wait until ticket `head` is published (device-memory poll)
-    while (bell <= head) {
+    uint64_t bell;
+    for (;;) {
       bell = ld_acquire_gpu(&dev->bell[worker]);
       if (bell > head) break;
       if (*reinterpret_cast<volatile uint32_t *>(&dev->stop)) return;
@@ -172,19 +204,28 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     SvcSlot *sl = myring + (head % ring);
     uint4 *page = mypages + (head % ring) * 256;
-    // header and page in one PCIe round trip (published before the doorbell):
-    // 64 threads x 4 coalesced 16-byte loads (1 KiB per instruction)
+    // page loads go out first; when `head` is the latest forwarded ticket its
+    // header is already in device memory, so the keystream is computed while
+    // the page bytes cross PCIe; otherwise the header comes from the slot
     uint4 d[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) d[j] = ld_volatile_v4(page + 64 * j + tid);
-    const uint64_t vaddr = *reinterpret_cast<volatile uint64_t *>(&sl->vaddr);
-    const uint32_t pid = *reinterpret_cast<volatile uint32_t *>(&sl->pid);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) tile[svc_swz(64 * j + tid)] = d[j];
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : : "memory");
+    uint64_t vaddr;
+    uint32_t pid;
+    const uint4 hd = ld_volatile_v4(&hdr[static_cast<uint64_t>(worker) * ring + head % ring]);
+    if (hd.w == static_cast<uint32_t>(head)) { // header forwarded with the bell
+      vaddr = static_cast<uint64_t>(hd.x) | (static_cast<uint64_t>(hd.y) << 32);
+      pid = hd.z;
+    } else {
+      vaddr = *reinterpret_cast<volatile uint64_t *>(&sl->vaddr);
+      pid = *reinterpret_cast<volatile uint32_t *>(&sl->pid);
+    }
     uint32_t x[16];
     const uint32_t sd[4] = {static_cast<uint32_t>(vaddr), static_cast<uint32_t>(vaddr >> 32), pid, tid};
     chacha_block<ROUNDS, 0>(x, k, sd, rm);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : : "memory");
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tile[svc_swz(64 * j + tid)] = d[j];
     named_bar(64);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2) : : "memory");
     // thread owns chunks 4*tid .. 4*tid+3 (its 64-byte block)
