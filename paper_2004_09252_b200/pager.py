@@ -66,8 +66,15 @@ class SlidingWindow:
     def resident(self, vaddr: int) -> bool:
         return vaddr in self._members
 
+    def clear(self) -> None:
+        self._queue.clear()
+        self._members.clear()
+
     def __len__(self) -> int:
         return len(self._queue)
+
+    def __iter__(self):
+        return iter(list(self._queue))
 
     def members(self) -> list[int]:
         return list(self._queue)
