@@ -89,7 +89,8 @@ struct Tuning {
                                        // 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced,
                                        // 4 = k_crypt_pages_tma, 5 = k_crypt_pages_async
   std::atomic<int> host_mode{2};       // large host batches: 0 = round-robin streams, 1 = zero-copy kernel
-                                       // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams
+                                       // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams,
+                                       // 3 = as 2 but the kernel writes pinned output directly
   std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
   Tuning() {
     kernel = env_int("PAGECRYPT_KERNEL", 0);
@@ -813,7 +814,11 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   // H2D -> kernel -> D2H in order on stream c % S.
   const int S = e->n_streams;
   const size_t C = e->chunk_pages;
-  const bool dedicated = tuning().host_mode.load() == 2 && S >= 3;
+  const int hm = tuning().host_mode.load();
+  const bool dedicated = (hm == 2 || hm == 3) && S >= 3;
+  // host_mode 3: the kernel stores each chunk's result straight into the
+  // caller's pinned output over PCIe (posted writes), so no D2H copy runs
+  const bool direct_out = hm == 3 && pin_out && dedicated;
   if (!pin_in || !pin_out) {
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
@@ -892,6 +897,13 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
     if (dedicated) {
       CU(cudaEventRecord(e->ev_h2d[s], sh));
       CU(cudaStreamWaitEvent(sk, e->ev_h2d[s], 0));
+    }
+    if (direct_out) {
+      int rc = launch_crypt(key, d, e->d_pages[s], static_cast<uint8_t *>(out_dev) + p0 * PC_PAGE_SIZE, m,
+                            rounds, sk, 3);
+      if (rc != PC_OK) return rc;
+      CU(cudaEventRecord(e->done[s], sk));
+      continue;
     }
     int rc = launch_crypt(key, d, e->d_pages[s], e->d_pages[s], m, rounds, sk);
     if (rc != PC_OK) return rc;
@@ -1636,7 +1648,7 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "host_mode")) {
-    if (value < 0 || value > 2) return fail(PC_EINVAL, "host_mode must be 0, 1 or 2");
+    if (value < 0 || value > 3) return fail(PC_EINVAL, "host_mode must be 0, 1, 2 or 3");
     t.host_mode = static_cast<int>(value);
     return PC_OK;
   }

@@ -190,7 +190,7 @@ class TestHostPath:
         got = pc.crypt_pages(dkey, BASE, 3, pages)
         assert np.array_equal(got, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=3, nthreads=8))
 
-    @pytest.mark.parametrize("host_mode", [0, 1, 2])
+    @pytest.mark.parametrize("host_mode", [0, 1, 2, 3])
     @pytest.mark.parametrize("n", [1, 64, 65, 9000])
     def test_pinned_torch(self, dkey, n, host_mode, knob):
         import torch
@@ -202,7 +202,7 @@ class TestHostPath:
         pc.crypt_pages(dkey, BASE, 4, src, out=dst)
         assert np.array_equal(dst.numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=4, nthreads=8))
 
-    @pytest.mark.parametrize("host_mode", [0, 1, 2])
+    @pytest.mark.parametrize("host_mode", [0, 1, 2, 3])
     def test_raw_key_host_with_descriptors(self, ref_pages, host_mode, knob):
         knob("host_mode", host_mode)
         r = ref_pages
@@ -220,7 +220,7 @@ class TestHostPath:
         pc.crypt_pages(dkey, BASE, 5, buf, out=buf)
         assert np.array_equal(buf, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=5, nthreads=8))
 
-    @pytest.mark.parametrize("host_mode", [0, 1, 2])
+    @pytest.mark.parametrize("host_mode", [0, 1, 2, 3])
     def test_in_place_pinned_with_pinned_descriptors(self, dkey, host_mode, knob):
         import torch
 
