@@ -537,6 +537,42 @@ k_slab_move(const uint32_t *__restrict__ key, PageDesc desc, const uint32_t *__r
   st_v4(dst, d0); st_v4(dst + 1, d1); st_v4(dst + 2, d2); st_v4(dst + 3, d3);
 }
 
+// Fused refault + evict for one fault (pc_store_swap): pages [0, n_get) of
+// the batch move slab -> staging through the cipher and their slots are
+// zeroed (a refault, orchestrator.py:190-198); pages [n_get, n) move
+// staging -> slab through the cipher (an eviction, orchestrator.py:230-238).
+// The two slot sets are disjoint (the store pops the eviction slots before
+// it frees the refault slots), so one launch does both.
+template <int ROUNDS>
+__global__ void __launch_bounds__(256)
+k_slab_swap(const uint32_t *__restrict__ key, PageDesc desc, const uint32_t *__restrict__ slots,
+            uint4 *slab, uint4 *staging, uint32_t n_get, uint64_t n_blocks) {
+  const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n_blocks) return;
+  const uint64_t page = g >> 6;
+  const uint32_t blk = static_cast<uint32_t>(g & 63);
+  const bool get = page < n_get;
+  uint4 *sp = slab + static_cast<uint64_t>(__ldg(slots + page)) * 256 + blk * 4;
+  uint4 *tp = staging + g * 4;
+  const uint4 *src = get ? sp : tp;
+  uint4 *dst = get ? tp : sp;
+  uint4 d0 = ld_v4(src), d1 = ld_v4(src + 1), d2 = ld_v4(src + 2), d3 = ld_v4(src + 3);
+  if (get) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    st_v4(sp, z); st_v4(sp + 1, z); st_v4(sp + 2, z); st_v4(sp + 3, z);
+  }
+  uint32_t k[8], s[4], x[16];
+  load_key(key, k);
+  page_seed(desc, page, s);
+  s[3] = blk;
+  chacha_block<ROUNDS, 0>(x, k, s, RotMul{});
+  d0.x ^= x[0];  d0.y ^= x[1];  d0.z ^= x[2];  d0.w ^= x[3];
+  d1.x ^= x[4];  d1.y ^= x[5];  d1.z ^= x[6];  d1.w ^= x[7];
+  d2.x ^= x[8];  d2.y ^= x[9];  d2.z ^= x[10]; d2.w ^= x[11];
+  d3.x ^= x[12]; d3.y ^= x[13]; d3.z ^= x[14]; d3.w ^= x[15];
+  st_v4(dst, d0); st_v4(dst + 1, d1); st_v4(dst + 2, d2); st_v4(dst + 3, d3);
+}
+
 // Zero the given slab slots (freed store entries are wiped, store.py:86-92).
 __global__ void __launch_bounds__(256)
 k_slab_wipe(const uint32_t *__restrict__ slots, uint4 *slab, uint64_t n_chunks) {

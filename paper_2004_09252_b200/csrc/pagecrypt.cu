@@ -1205,6 +1205,7 @@ cudaError_t touch_rounds() {
   acc(touch(pc::k_service<R>));
   acc(touch(pc::k_slab_move<R, 0>));
   acc(touch(pc::k_slab_move<R, 1>));
+  acc(touch(pc::k_slab_swap<R>));
   return e;
 }
 } // namespace

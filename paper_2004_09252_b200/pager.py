@@ -9,6 +9,9 @@ encrypt it and store it -- two synchronous single-page crypto calls per
 fault.  ``WindowPager`` keeps those semantics and adds ``fault_batch``: all
 faults of a batch are resolved with ONE ``refault_many`` (decrypt out of
 HBM) and ONE ``evict_many`` (encrypt into HBM), so the GPU sees real batches.
+When the evicted pages were all resident before the batch (always, for a
+single fault with a full window), refault and eviction are independent and
+run as ONE ``DevicePageStore.swap`` -- one GPU round trip per fault.
 
 A batch is equivalent to faulting its pages one by one in order (checked in
 ``tests/test_gpu_pager.py``): a page evicted by a later fault of the same
@@ -31,6 +34,7 @@ from .errors import ContractViolation
 from .store import DevicePageStore
 
 PAGE_SIZE = 4096
+FUSED_MAX = 64  # pages per pc_store_swap launch (refaults + evictions)
 
 
 class SlidingWindow:
@@ -144,37 +148,59 @@ class WindowPager:
         out = np.zeros((k, PAGE_SIZE), dtype=np.uint8)  # first touch: zero pages
         if not k:
             return out
-        # 1. refaults: one decrypt-out-of-HBM batch (entries are removed)
         refault_idx = [i for i, v in enumerate(vlist) if self.store.contains(client, v)]
-        if refault_idx:
-            plains = self.store.refault_many(client, [vlist[i] for i in refault_idx])
-            out[refault_idx] = plains
-            m.decrypt_ops += len(refault_idx)
-            m.gpu_batches += 1
-        m.first_touch_faults += k - len(refault_idx)
-        m.faults += k
-        # 2. window admission in fault order; collect evictions
         batch_pos = {v: i for i, v in enumerate(vlist)}
+        # window admission in fault order (host state only); collect evictions
+        saved = (deque(win._queue), set(win._members))
         evicted: list[int] = []
         for v in vlist:
             e = win.admit(v)
             if e is not None:
                 evicted.append(e)
-        if not evicted:
-            return out
-        # 3. evictions: pages resident before the batch come back from the
-        #    client; pages faulted in by this batch carry their resolved bytes
-        from_client = [e for e in evicted if e not in batch_pos]
-        plain_ev = np.empty((len(evicted), PAGE_SIZE), dtype=np.uint8)
-        if from_client:
-            got = np.ascontiguousarray(self.fetch_evicted(client, from_client), dtype=np.uint8)
-            got = got.reshape(len(from_client), PAGE_SIZE)
-            row = {e: j for j, e in enumerate(from_client)}
-        for j, e in enumerate(evicted):
-            plain_ev[j] = out[batch_pos[e]] if e in batch_pos else got[row[e]]
-        self.store.evict_many(client, evicted, plain_ev)
-        plain_ev.fill(0)  # scratch_evict.wipe(), orchestrator.py:239
+        try:
+            if (refault_idx and evicted and len(refault_idx) + len(evicted) <= FUSED_MAX
+                    and not any(e in batch_pos for e in evicted)):
+                # the common single fault: the evicted pages were resident
+                # before the batch, so refault and eviction are independent
+                # -> one GPU round trip (pc_store_swap)
+                plain_ev = self._from_client(client, evicted)
+                out[refault_idx] = self.store.swap(client, [vlist[i] for i in refault_idx], evicted, plain_ev)
+                plain_ev.fill(0)  # scratch_evict.wipe(), orchestrator.py:239
+                m.gpu_batches += 1
+            else:
+                # 1. refaults: one decrypt-out-of-HBM batch (entries are removed)
+                if refault_idx:
+                    out[refault_idx] = self.store.refault_many(client, [vlist[i] for i in refault_idx])
+                    m.gpu_batches += 1
+                # 2. evictions: pages resident before the batch come back from
+                #    the client; pages faulted in by this batch carry their
+                #    resolved bytes
+                if evicted:
+                    from_client = [e for e in evicted if e not in batch_pos]
+                    got = self._from_client(client, from_client)
+                    row = {e: j for j, e in enumerate(from_client)}
+                    plain_ev = np.empty((len(evicted), PAGE_SIZE), dtype=np.uint8)
+                    for j, e in enumerate(evicted):
+                        plain_ev[j] = out[batch_pos[e]] if e in batch_pos else got[row[e]]
+                    self.store.evict_many(client, evicted, plain_ev)
+                    plain_ev.fill(0)
+                    got.fill(0)
+                    m.gpu_batches += 1
+        except BaseException:
+            win._queue, win._members = saved
+            raise
+        m.decrypt_ops += len(refault_idx)
+        m.first_touch_faults += k - len(refault_idx)
+        m.faults += k
         m.evictions += len(evicted)
         m.encrypt_ops += len(evicted)
-        m.gpu_batches += 1
         return out
+
+    def _from_client(self, client, vaddrs: list[int]) -> np.ndarray:
+        """Pull evicted pages back from the client (client.py:251-265)."""
+        if not vaddrs:
+            return np.empty((0, PAGE_SIZE), dtype=np.uint8)
+        # a private copy (the server's scratch_evict, orchestrator.py:230-239):
+        # it is wiped after use, the caller's buffer is not touched
+        got = np.array(self.fetch_evicted(client, vaddrs), dtype=np.uint8, copy=True, order="C")
+        return got.reshape(len(vaddrs), PAGE_SIZE)

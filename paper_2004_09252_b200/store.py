@@ -18,7 +18,9 @@ slots are wiped), plus the fused paths the B200 makes possible:
 * ``refault(client, vaddr)``: the ciphertext is decrypted on the way out of
   HBM and the entry removed (``orchestrator.py:190-198``);
 * ``evict_many`` / ``refault_many``: the same for whole batches, one
-  pipelined transfer per batch.
+  pipelined transfer per batch;
+* ``swap(client, refault_vaddrs, evict_vaddrs, evict_plains)``: a whole
+  fault (refault + eviction) in one GPU round trip (``pc_store_swap``).
 
 Only ``client.pid`` enters the cipher seed, as in the reference worker
 (``workers.py:137``); the index is keyed by (pid, epoch).
@@ -189,4 +191,25 @@ class DevicePageStore:
             raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
         self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
                    out.ctypes.data, 1, 1)
+        return out
+
+    def swap(self, client, refault_vaddrs, evict_vaddrs, evict_plains, out: np.ndarray | None = None) -> np.ndarray:
+        """Refault ``refault_vaddrs`` (decrypt out of HBM, remove) and evict
+        ``evict_plains`` to ``evict_vaddrs`` (encrypt into HBM) -- one fault of
+        the orchestrator (``orchestrator.py:175-240``) -- in one GPU round trip
+        for up to 64 pages in total.  Same result as ``refault_many`` then
+        ``evict_many``.  Returns the refaulted plaintexts."""
+        self._need_key()
+        gv = self._vaddrs(refault_vaddrs)
+        pv = self._vaddrs(evict_vaddrs)
+        arr = evict_plains if isinstance(evict_plains, np.ndarray) else np.asarray(evict_plains)
+        arr = np.ascontiguousarray(arr, dtype=np.uint8).reshape(-1, PAGE_SIZE)
+        if arr.shape[0] != pv.size:
+            raise ContractViolation(f"{pv.size} vaddrs for {arr.shape[0]} pages")
+        if out is None:
+            out = np.empty((gv.size, PAGE_SIZE), dtype=np.uint8)
+        elif out.nbytes != gv.size * PAGE_SIZE or not out.flags.c_contiguous:
+            raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
+        self._call("pc_store_swap", self._h, _cid(client), client.pid, gv.ctypes.data, gv.size,
+                   out.ctypes.data, pv.ctypes.data, pv.size, arr.ctypes.data)
         return out

@@ -114,6 +114,34 @@ def test_single_fault_matches_orchestrator_flow(dkey):
     assert store.lookup(C, 0x2000) == O.crypt_page(KEY, 0x2000, C.pid, b"\x22" * 4096)
     m = pager.metrics[C]
     assert (m.faults, m.first_touch_faults, m.decrypt_ops, m.evictions) == (3, 2, 1, 2)
+    assert m.gpu_batches == 2  # the refaulting fault is ONE pc_store_swap round trip
+
+
+def test_failed_fault_leaves_window_and_store_unchanged(dkey):
+    store = DevicePageStore(16, dkey)
+    mem = {}
+    fail = [False]
+
+    def fetch(c, vs):
+        if fail[0]:
+            raise RuntimeError("client unreachable")
+        return np.stack([np.frombuffer(mem.pop(v), np.uint8) for v in vs])
+
+    pager = WindowPager(store, fetch, 2)
+    pager.register(C)
+    for v in (0x1000, 0x2000, 0x3000):  # 0x1000 evicted by the third fault
+        pager.fault(C, v)
+        mem[v] = bytes([v >> 12]) * 4096
+    mem.pop(0x1000, None)
+    fail[0] = True
+    with pytest.raises(RuntimeError):
+        pager.fault(C, 0x1000)  # would refault 0x1000 and evict 0x2000
+    assert pager.window(C) == [0x2000, 0x3000]
+    assert store.contains(C, 0x1000) and not store.contains(C, 0x2000)
+    fail[0] = False
+    assert pager.fault(C, 0x1000) == b"\x01" * 4096
+    assert pager.window(C) == [0x3000, 0x1000]
+    assert store.lookup(C, 0x2000) == O.crypt_page(KEY, 0x2000, C.pid, b"\x02" * 4096)
 
 
 def test_contract_errors(dkey):

@@ -179,3 +179,72 @@ def test_single_page_fused_paths(dkey):
     assert s.contains(C1, 0x1000)
     with pytest.raises(StoreFull):
         s.evict_many(C1, [0x10000 * i for i in range(1, 9)], np.zeros((8, 4096), np.uint8))
+
+
+# ---- pc_store_swap: one fault (refault + eviction) in one GPU round trip ----
+
+
+@pytest.mark.parametrize("rounds", [8, 12, 20])
+def test_swap_matches_refault_then_evict(dkey, rounds):
+    """swap == refault_many followed by evict_many: same plaintexts out, same
+    ciphertext stored (the oracle's), same slot accounting."""
+    rng = np.random.default_rng(rounds)
+    s = DevicePageStore(256, dkey, rounds=rounds)
+    c = ClientId(77, 3)
+    va = [0x1_0000_0000 + 4096 * i for i in range(40)]
+    plains = rng.integers(0, 256, size=(40, 4096), dtype=np.uint8)
+    s.evict_many(c, va[:20], plains[:20])
+    for n_get, n_put in ((1, 1), (0, 3), (5, 0), (7, 9), (20, 20)):
+        get = [v for v in va if s.contains(c, v)][:n_get]
+        put = [v for v in va if not s.contains(c, v)][:n_put]
+        want_out = np.stack([plains[va.index(v)] for v in get]) if get else np.empty((0, 4096), np.uint8)
+        put_pl = np.stack([plains[va.index(v)] for v in put]) if put else np.empty((0, 4096), np.uint8)
+        free0 = s.free_slots
+        got = s.swap(c, get, put, put_pl)
+        assert np.array_equal(got, want_out)
+        assert s.free_slots == free0 + len(get) - len(put)
+        assert not any(s.contains(c, v) for v in get)
+        if put:
+            want_ct = C.crypt_pages(KEY, np.array(put, np.uint64), c.pid, put_pl, rounds=rounds)
+            for v, ct in zip(put, want_ct):
+                assert s.lookup(c, v) == ct.tobytes()
+
+
+def test_swap_same_vaddr_out_and_back_in(dkey):
+    s = DevicePageStore(4, dkey)
+    p1, p2 = page(1), page(2)
+    s.evict(C1, 0x5000, p1)
+    got = s.swap(C1, [0x5000], [0x5000], np.frombuffer(p2, np.uint8).reshape(1, 4096))
+    assert got[0].tobytes() == p1
+    assert s.refault(C1, 0x5000) == p2
+    assert s.free_slots == 4
+
+
+def test_swap_full_slab_falls_back_and_zeroes_freed_slots(dkey):
+    s = DevicePageStore(2, dkey)
+    s.evict(C1, 0x1000, page(1))
+    s.evict(C1, 0x2000, page(2))
+    # no free slot before the refault frees one: runs as refault then evict
+    got = s.swap(C1, [0x1000], [0x3000], np.frombuffer(page(3), np.uint8).reshape(1, 4096))
+    assert got[0].tobytes() == page(1)
+    assert s.refault(C1, 0x3000) == page(3)
+    assert s.refault(C1, 0x2000) == page(2)
+    assert s.free_slots == 2
+
+
+def test_swap_is_all_or_nothing(dkey):
+    s = DevicePageStore(16, dkey)
+    s.evict(C1, 0x1000, page(1))
+    s.evict(C1, 0x2000, page(2))
+    one = np.frombuffer(page(9), np.uint8).reshape(1, 4096)
+    with pytest.raises(ContractViolation):  # refault of a missing page
+        s.swap(C1, [0x1000, 0x9000], [0x3000], one)
+    with pytest.raises(ContractViolation):  # eviction onto a stored page
+        s.swap(C1, [0x1000], [0x2000], one)
+    with pytest.raises(ContractViolation):  # unaligned eviction vaddr
+        s.swap(C1, [0x1000], [0x3001], one)
+    with pytest.raises(ContractViolation):  # duplicate refault
+        s.swap(C1, [0x1000, 0x1000], [], np.empty((0, 4096), np.uint8))
+    assert s.contains(C1, 0x1000) and s.contains(C1, 0x2000) and not s.contains(C1, 0x3000)
+    assert s.free_slots == 14
+    assert s.refault(C1, 0x1000) == page(1)
