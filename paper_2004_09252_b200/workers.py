@@ -188,8 +188,27 @@ class WorkerPool:
                 self._pending.pop((w, t), None)
 
     def crypt(self, client, vaddr: int, direction: str, page) -> None:
-        """Submit and wait: the synchronous fault-path helper (workers.py:227-229)."""
-        self.submit(client, vaddr, direction, page).wait()
+        """Submit and wait: the synchronous fault-path helper (workers.py:227-229).
+        Same checks and errors as ``submit(...).wait()``, in ONE native call
+        (pc_service_crypt) with no per-request bookkeeping: the page is
+        transformed in place before this returns."""
+        if self._shut_down:
+            raise PoolError("submit on a shut-down pool")
+        if direction not in ("encrypt", "decrypt"):
+            raise ContractViolation(f"bad direction {direction!r}")
+        arr = _page_view(page)
+        if arr.size != PAGE_SIZE:
+            raise ContractViolation("crypto requests operate on whole pages")
+        _check_vaddr_int(vaddr)
+        _check_pid_int(client.pid)
+        if not arr.flags.writeable:
+            raise ContractViolation("page buffer must be writable (it is transformed in place)")
+        ptr = arr.ctypes.data
+        rc = self._lib.pc_service_crypt(self._svc, self.route(client), vaddr, client.pid, ptr, ptr, -1)
+        if rc != _native.PC_OK:
+            if rc == _native.PC_ETIMEOUT:
+                raise PoolError("timed out waiting for crypto completion")
+            _native.check(rc)
 
     @property
     def in_flight(self) -> int:
