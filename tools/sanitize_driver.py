@@ -40,7 +40,7 @@ def main():
                                      torch.from_numpy(pi.view(np.int32)).cuda(), torch.from_numpy(pages).cuda(), rounds=r)
                 assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, va, pi, pages, rounds=r)), (kern, r)
         _native.tune("kernel", 0)
-        for hm in (0, 1, 2):
+        for hm in (0, 1, 2, 3):
             _native.tune("host_mode", hm)
             src = torch.from_numpy(np.concatenate([pages] * 3)).pin_memory()
             out = torch.empty_like(src).pin_memory()
@@ -55,6 +55,11 @@ def main():
         st.evict_many(ClientId(5, 0), va[:20], pages[:20])
         back = st.refault_many(ClientId(5, 0), va[:20])
         assert np.array_equal(back, pages[:20])
+        # one fused fault (refault + eviction in one launch, pc_store_swap)
+        st.evict_many(ClientId(5, 0), va[:3], pages[:3])
+        got = st.swap(ClientId(5, 0), va[:3], va[3:7], pages[3:7])
+        assert np.array_equal(got, pages[:3])
+        assert np.array_equal(st.refault_many(ClientId(5, 0), va[3:7]), pages[3:7])
     pool = WorkerPool(n_workers=3, keysource=lambda m: KEY)
     for i in range(12):
         buf = bytearray(pages[i].tobytes())
