@@ -156,7 +156,11 @@ unsigned pages_grid(size_t n_pages) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
     occ[dev] = o > 0 ? o : 1;
   }
-  const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : occ[dev];
+  // v5 at ChaCha12 runs best at 2 of its 4 resident CTAs per SM: 2835 vs
+  // 2774 GB/s through bench.py (profiles/r01_ctas_ab.txt) -- fewer
+  // concurrent page streams, same ALU feed (ILP 4 per thread)
+  const int dflt = (Variant == 2 && R == 12) ? std::min(occ[dev], 2) : occ[dev];
+  const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : dflt;
   const uint64_t want = static_cast<uint64_t>(sms[dev]) * per_sm;
   const uint64_t slots = (n_pages + 3) / 4;
   return static_cast<unsigned>(std::min<uint64_t>(want, slots));
