@@ -425,7 +425,7 @@ def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
     for n in (1, 2, 4, 8, 16, 32, 64):
         src = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8).pin_memory()
         dst = torch.empty_like(src).pin_memory()
-        for _ in range(20):
+        for _ in range(300):  # ~5 ms: lets the SM clock leave its idle state first
             pc.crypt_pages(key, BASE_VADDR, 1, src, out=dst)
         ts = []
         for _ in range(reps):

@@ -57,6 +57,40 @@ def _addr_of_readonly(buf) -> tuple[int, Any]:
     return arr.ctypes.data, arr
 
 
+_Key = ctypes.c_char * KEY_SIZE
+
+
+def _ptr(buf, ctype):
+    """(argument, keepalive): something ctypes passes as a c_void_p to buf's
+    bytes, without copying them (a copy of key material could not be wiped).
+    bytes and bytearray take the cheap paths; anything else goes through numpy."""
+    if type(buf) is bytes:
+        return buf, buf
+    if type(buf) is bytearray:
+        return ctype.from_buffer(buf), buf
+    arr = np.frombuffer(buf, dtype=np.uint8) if not isinstance(buf, np.ndarray) else buf
+    if not arr.flags.c_contiguous:
+        raise ContractViolation("buffer must be C-contiguous")
+    return arr.ctypes.data, arr
+
+
+def _addr(arr: np.ndarray) -> int:
+    """Address of a non-empty C-contiguous array (``arr.ctypes.data`` costs
+    ~2 us; a ctypes view of a writable buffer ~0.8 us)."""
+    if arr.flags.writeable:
+        return ctypes.addressof(ctypes.c_char.from_buffer(arr))
+    return arr.ctypes.data
+
+
+def raw_key_arg(key):
+    """(argument, keepalive) for the raw-key (caller-key) mode of the C ABI:
+    32 key bytes from MasterKey / bytes / bytearray / memoryview, validated,
+    passed by address without a copy."""
+    kv = key_bytes(key)
+    obj = kv.obj
+    return _ptr(obj if type(obj) in (bytes, bytearray) and len(obj) == KEY_SIZE else kv, _Key)
+
+
 class DeviceKey:
     """A 256-bit master key resident in one GPU's memory (the key slot)."""
 
@@ -157,30 +191,35 @@ class Engine:
         _check_rounds(rounds)
         v_arr, vaddr0 = _host_vaddrs(vaddrs, n)
         p_arr, pid0 = _host_pids(pids, n)
-        keep = []
         if isinstance(key, DeviceKey):
             if key.device != self.device:
                 raise ContractViolation(f"key on device {key.device}, engine on {self.device}")
-            kh, raw = key.handle, None
+            kh, raw = key.handle, (None, None)
         else:
-            kh = None
-            raw, k = _addr_of_readonly(key_bytes(key))
-            keep.append(k)
-        _native.call(
-            "pc_crypt_pages_host", self.handle, kh, raw,
+            kh, raw = None, raw_key_arg(key)
+        rc = _native.load().pc_crypt_pages_host(
+            self.handle, kh, raw[0],
             None if v_arr is None else v_arr.ctypes.data,
             None if p_arr is None else p_arr.ctypes.data,
             vaddr0, pid0, src_addr, dst_addr, n, rounds,
         )
+        if rc:
+            _native.check(rc)
 
 
 _engines: dict[int, Engine] = {}
 _engines_lock = threading.Lock()
 
 
+_default_device: int | None = None
+
+
 def default_engine(device: int | None = None) -> Engine:
+    global _default_device
     if device is None:
-        device = int(os.environ.get("PAGECRYPT_DEVICE", "0"))
+        if _default_device is None:
+            _default_device = int(os.environ.get("PAGECRYPT_DEVICE", "0"))
+        device = _default_device
     eng = _engines.get(device)
     if eng is None:
         with _engines_lock:
@@ -310,7 +349,9 @@ def _crypt_pages_host(key, vaddrs, pids, pages, rounds, out, engine):
         oarr = out if isinstance(out, np.ndarray) else np.frombuffer(out, dtype=np.uint8)
         if oarr.nbytes != n * PAGE_SIZE or not oarr.flags.writeable:
             raise ContractViolation("out must be a writable buffer of the same size")
-        src, dst = arr.ctypes.data, oarr.ctypes.data
+        if n == 0:
+            return out
+        src, dst = _addr(arr), _addr(oarr)
         keep = (arr, oarr)
     if n == 0:
         return out
