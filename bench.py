@@ -375,6 +375,9 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1:
         cpu = cpu_port_rate(args.rounds, args.cpu_seconds, len(os.sched_getaffinity(0)))
+        one = cpu_port_rate(args.rounds, max(0.5, args.cpu_seconds / 5), 1, pages_per_batch=256)
+        cpu["single_thread"] = {"value": round(one["value"], 4), "unit": "GB/s", "cores": 1,
+                                "sample": one["sample"]}
 
     key.destroy()
     if rank == 0:
