@@ -271,16 +271,20 @@ def main() -> None:
     def step(rounds):
         pc.crypt_pages(key, vaddr0, 1, pages, out=out, rounds=rounds, stream=stream, check=False)
 
+    launches = {}
+
     def timed(rounds, steps, warmup):
         for _ in range(warmup):
             step(rounds)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _native.tune_get("launches")
         e0.record(stream)
         for _ in range(steps):
             step(rounds)
         e1.record(stream)
         e1.synchronize()
+        launches[rounds] = _native.tune_get("launches") - l0  # counted by the library itself
         barrier()
         return e0.elapsed_time(e1)  # ms on the launching stream
 
@@ -345,16 +349,17 @@ def main() -> None:
     for _ in range(3):
         pc.crypt_pages(key, vaddr0, 1, host_in, out=host_out, rounds=args.rounds, engine=eng)
     barrier()
+    l0 = _native.tune_get("launches")
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         pc.crypt_pages(key, vaddr0, 1, host_in, out=host_out, rounds=args.rounds, engine=eng)
     e2e_s = time.perf_counter() - t0
+    e2e_launches = _native.tune_get("launches") - l0
     e2e_s = max_over_ranks(e2e_s, device=red_dev)
     e2e = {"value": round(world * bytes_per_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": bytes_per_step, "d2h_bytes_per_step": bytes_per_step,
            "steps": e2e_steps, "path": "crypt_pages(DeviceKey, pinned torch CPU tensors) -> "
            f"pc_crypt_pages_host, {eng.n_streams} streams x {eng.chunk_pages}-page chunks"}
-    chunks = -(-n // eng.chunk_pages)
 
     extras = {}
     if not args.no_extras:
@@ -388,8 +393,9 @@ def main() -> None:
             "data": "synthetic (uniform random pages, seed 1+rank; key from DeviceKey.generate)",
             "config": workload_config(args, world),
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps + e2e_steps * chunks,
-            "gpu_launches_detail": {"device_timed": args.steps, "e2e_timed": e2e_steps * chunks},
+            "gpu_launches": launches[args.rounds] + e2e_launches,
+            "gpu_launches_detail": {"device_timed": launches[args.rounds], "e2e_timed": e2e_launches,
+                                    "source": "libpagecrypt's own launch counter (pc_tune_get(\"launches\"))"},
             "clocks": clk.summary(), "gpu": torch.cuda.get_device_name(dev),
             "extras": extras,
         }

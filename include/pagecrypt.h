@@ -226,7 +226,9 @@ int pc_host_unregister(void *p);
 int pc_intpeak(int device, int kind, double *ops_per_s);
 /* Process-wide knobs: "rotmask" (compiled FMA-pipe rotate pattern of the
  * crypt kernel, see chacha.cuh), "small_mode" (0 staged copies / 1 zero-copy
- * for small host batches); pc_tune_get also reads "small_max". */
+ * for small host batches), "small_max", "kernel" (0 auto, 1..5 page-kernel
+ * variant), "host_mode" (0..3 host pipeline), "ctas_per_sm"; pc_tune_get
+ * also reads "launches", the number of kernels this library has launched. */
 int pc_tune(const char *knob, int64_t value);
 int pc_tune_get(const char *knob, int64_t *value);
 

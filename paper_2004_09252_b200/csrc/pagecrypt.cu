@@ -101,6 +101,12 @@ struct Tuning {
     small_max = static_cast<size_t>(env_int("PAGECRYPT_SMALL_MAX", 64));
   }
 };
+// Kernel launches issued by this library (all kernels, all devices), read
+// through pc_tune_get("launches"): bench.py reports the launches inside its
+// timed regions from it.
+std::atomic<uint64_t> g_launches{0};
+inline void counted(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 Tuning &tuning() {
   static Tuning t;
   return t;
@@ -122,6 +128,7 @@ void launch_crypt_rm(const uint32_t *key, const pc::PageDesc &d, const void *in,
   const dim3 grid(static_cast<unsigned>((n_blocks + 255) / 256));
   pc::k_crypt_blocks<R, M><<<grid, block, 0, st>>>(key, d, static_cast<const uint4 *>(in),
                                                    static_cast<uint4 *>(out), n_blocks, kRotMul);
+  counted();
 }
 
 template <int R>
@@ -171,9 +178,10 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
                     void *out, size_t n_pages, cudaStream_t st) {
   auto i4 = static_cast<const uint4 *>(in);
   auto o4 = static_cast<uint4 *>(out);
-  if (kern == 3)
+  if (kern == 3) {
     pc::k_crypt_pages_coalesced<R><<<pages_grid<R, 1>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
-  else if (kern == 5) {
+    counted();
+  } else if (kern == 5) {
     // 32-bit page loop: split batches at 2^30 pages (4 TiB)
     constexpr size_t kMax = size_t(1) << 30;
     for (size_t p0 = 0; p0 < n_pages; p0 += kMax) {
@@ -185,10 +193,13 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
         pc::k_crypt_pages_async<R, true><<<grid, 256, 0, st>>>(key, dd, i4 + p0 * 256, o4 + p0 * 256, m);
       else
         pc::k_crypt_pages_async<R, false><<<grid, 256, 0, st>>>(key, dd, i4 + p0 * 256, o4 + p0 * 256, m);
+      counted();
     }
   }
-  else
+  else {
     pc::k_crypt_pages<R><<<pages_grid<R, 0>(n_pages), 256, 0, st>>>(key, d, i4, o4, n_pages);
+    counted();
+  }
 }
 
 // ---- v4: TMA pipeline --------------------------------------------------------
@@ -251,6 +262,7 @@ int launch_tma_r(const uint32_t *key, const pc::PageDesc &d, const void *in, voi
     const uint64_t slots = (m + 3) / 4;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(static_cast<uint64_t>(sms[dev]) * per_sm, slots));
     kfn<<<grid, 256, kTmaSmem, st>>>(tin, tout, key, dd, m);
+    counted();
     CU(cudaGetLastError());
   }
   return PC_OK;
@@ -305,6 +317,7 @@ int launch_keystream(const uint32_t *key, const uint32_t *seeds, size_t k, uint3
     case 12: pc::k_keystream_seeds<12><<<grid, block, 0, st>>>(key, seeds, k, out); break;
     default: pc::k_keystream_seeds<20><<<grid, block, 0, st>>>(key, seeds, k, out); break;
   }
+  counted();
   CU(cudaGetLastError());
   return PC_OK;
 }
@@ -490,6 +503,7 @@ int key_create(int device, const uint8_t *src, bool derive, pc_key **out) {
     cudaError_t e = cudaMemcpyAsync(dst, sc.h, 32, cudaMemcpyHostToDevice, k->kst);
     if (e == cudaSuccess && derive) {
       pc::k_keygen<<<1, 1, 0, k->kst>>>(k->d_words + 8, k->d_words);
+      counted();
       e = cudaGetLastError();
       if (e == cudaSuccess) e = cudaMemsetAsync(k->d_words + 8, 0, 32, k->kst);
     }
@@ -983,6 +997,7 @@ void launch_slab_r(int dir, const uint32_t *key, const pc::PageDesc &d, const ui
   auto sg = static_cast<uint4 *>(staging);
   if (dir == 0) pc::k_slab_move<R, 0><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb, false);
   else pc::k_slab_move<R, 1><<<grid, 256, 0, st>>>(key, d, slots, sl, sg, nb, wipe_src);
+  counted();
 }
 } // namespace
 
@@ -1132,6 +1147,7 @@ extern "C" int pc_slab_wipe(pc_engine *e, void *slab, size_t slab_pages, const u
     CU(cudaMemcpyAsync(d_slots, e->h_desc[0] + C * 12, m * 4, cudaMemcpyHostToDevice, st));
     const uint64_t chunks = static_cast<uint64_t>(m) * 256;
     pc::k_slab_wipe<<<static_cast<unsigned>((chunks + 255) / 256), 256, 0, st>>>(d_slots, static_cast<uint4 *>(slab), chunks);
+    counted();
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(st)); // h_desc[0] is reused by the next piece
   }
@@ -1247,6 +1263,7 @@ int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key
     case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr); break;
     default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr); break;
   }
+  counted();
   CU(cudaGetLastError());
   return PC_OK;
 }
@@ -1602,6 +1619,7 @@ int pc_intpeak(int device, int kind, double *ops_per_s) {
       case 6: pc::k_intpeak<6><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
       default: pc::k_intpeak<7><<<grid, block, 0, st>>>(1u, kRotMul, it, sink); break;
     }
+    counted();
   };
   cudaEvent_t a, b;
   CU(cudaEventCreate(&a));
@@ -1673,6 +1691,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   else if (!std::strcmp(knob, "small_max")) *value = static_cast<int64_t>(t.small_max.load());
   else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
   else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;
+  else if (!std::strcmp(knob, "launches")) *value = static_cast<int64_t>(g_launches.load());
   else if (!std::strcmp(knob, "ctas_per_sm")) *value = t.ctas_per_sm;
   else return fail(PC_EINVAL, "unknown knob '%s'", knob);
   return PC_OK;
