@@ -100,7 +100,10 @@ int pc_crypt_pages_dev(const pc_key *key, const uint64_t *vaddrs, const uint32_t
  * Same result over host buffers.  Pinned buffers (pc_host_alloc /
  * pc_host_register / torch pin_memory) stream through the engine's staging
  * ring on several CUDA streams so H2D, cipher and D2H overlap; small
- * batches take a single-launch path.  vaddrs/pids: host arrays or NULL.
+ * batches take a single-launch path.  in/out may also be device memory of
+ * any GPU: pages on the engine's own GPU (contiguous vaddrs, scalar pid,
+ * DeviceKey) run as one in-place launch; pages on another GPU stream through
+ * the engine's ring by peer copies (NVLink) instead of PCIe.  vaddrs/pids: host arrays or NULL.
  * Synchronous: returns when out holds the result.  `key` may be NULL when
  * raw_key is given (caller-key mode: the engine copies raw_key into a device
  * slot for this call and zeroes it before returning). */
@@ -113,7 +116,8 @@ int pc_crypt_pages_host(pc_engine *eng, const pc_key *key, const uint8_t *raw_ke
 /* ---- (vi) multi-device partition ---------------------------------------
  * Contiguous page range [g*n/G, (g+1)*n/G) per engine g, each with its own
  * device key (keys[g] must live on engines[g]'s device); no collective.
- * Host buffers; one host thread per device; synchronous. */
+ * Host buffers, or device memory of one GPU (the other GPUs' ranges cross
+ * NVLink peer-to-peer); one host thread per device; synchronous. */
 int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, int n_dev,
                          const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
                          uint32_t pid0, const void *in, void *out, size_t n, int rounds);

@@ -92,6 +92,8 @@ struct Tuning {
                                        // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams,
                                        // 3 = as 2 but the kernel writes pinned output directly
   std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
+  std::atomic<int> dev_direct{1};      // device pages on the engine's own GPU: 1 = one in-place launch,
+                                       // 0 = stage through the engine's slots (tests the peer path on 1 GPU)
   Tuning() {
     kernel = env_int("PAGECRYPT_KERNEL", 0);
     host_mode = env_int("PAGECRYPT_HOST_MODE", 2);
@@ -333,6 +335,18 @@ bool pinned_alias(const void *p, void **dev) {
   }
   if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return false;
   *dev = a.devicePointer;
+  return true;
+}
+
+// Is p device memory (of any GPU; managed memory counts)?  *device = its GPU.
+bool device_memory(const void *p, int *device) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return false;
+  *device = a.device;
   return true;
 }
 
@@ -809,10 +823,14 @@ int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, cons
 int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const uint32_t *pids,
                 uint64_t vaddr0, uint32_t pid0, const void *in, void *out, size_t n, int rounds) {
   void *in_dev = nullptr, *out_dev = nullptr;
-  const bool pin_in = pinned_alias(in, &in_dev);
-  const bool pin_out = pinned_alias(out, &out_dev);
+  int gin = -1, gout = -1;
+  // device memory (this GPU or a peer) is an endpoint like pinned memory:
+  // no bounce buffer, copies by UVA (peer copies over NVLink), but the
+  // zero-copy modes below only apply to mapped host memory
+  const bool pin_in = pinned_alias(in, &in_dev) || device_memory(in, &gin);
+  const bool pin_out = pinned_alias(out, &out_dev) || device_memory(out, &gout);
   const bool has_desc = vaddrs || pids;
-  if (tuning().host_mode.load() == 1 && pin_in && pin_out) {
+  if (tuning().host_mode.load() == 1 && in_dev && out_dev) {
     // zero-copy: one coalesced kernel streams the pages over PCIe itself
     // (GPU-initiated reads and posted writes, both directions at once)
     void *v_dev = nullptr, *p_dev = nullptr;
@@ -836,7 +854,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   const bool dedicated = (hm == 2 || hm == 3) && S >= 3;
   // host_mode 3: the kernel stores each chunk's result straight into the
   // caller's pinned output over PCIe (posted writes), so no D2H copy runs
-  const bool direct_out = hm == 3 && pin_out && dedicated;
+  const bool direct_out = hm == 3 && out_dev && dedicated;
   if (!pin_in || !pin_out) {
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
@@ -900,7 +918,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
       e->pool->memcpy(e->h_bounce[s], src, m * PC_PAGE_SIZE);
       src = e->h_bounce[s];
     }
-    CU(cudaMemcpyAsync(e->d_pages[s], src, m * PC_PAGE_SIZE, cudaMemcpyHostToDevice, sh));
+    CU(cudaMemcpyAsync(e->d_pages[s], src, m * PC_PAGE_SIZE, cudaMemcpyDefault, sh));
     pc::PageDesc d{nullptr, nullptr, vaddr0 + 4096ull * p0, pid0};
     if (vaddrs) {
       std::memcpy(e->h_desc[s], vaddrs + p0, m * 8);
@@ -930,7 +948,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
       CU(cudaStreamWaitEvent(sd, e->ev_k[s], 0));
     }
     uint8_t *dst = pin_out ? dst_b + p0 * PC_PAGE_SIZE : e->h_bounce[s];
-    CU(cudaMemcpyAsync(dst, e->d_pages[s], m * PC_PAGE_SIZE, cudaMemcpyDeviceToHost, sd));
+    CU(cudaMemcpyAsync(dst, e->d_pages[s], m * PC_PAGE_SIZE, cudaMemcpyDefault, sd));
     CU(cudaEventRecord(e->done[s], sd));
   }
   const size_t first_pending = n_chunks > static_cast<size_t>(S) ? n_chunks - S : 0;
@@ -960,8 +978,19 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
   std::lock_guard<std::mutex> lk(e->mu);
   DeviceGuard g(e->device);
   CU(g.err);
-  if (n <= tuning().small_max)
+  int gin = -1, gout = -1;
+  const bool din = device_memory(in, &gin), dout = device_memory(out, &gout);
+  if (n <= tuning().small_max && !din && !dout)
     return crypt_small(e, raw_key ? nullptr : key->d_words, raw_key, vaddrs, pids, vaddr0, pid0, in, out, n, rounds);
+  if (din && dout && gin == e->device && gout == e->device && !vaddrs && !pids && !raw_key &&
+      tuning().dev_direct.load()) {
+    // pages already in this GPU's memory: one in-place launch, no staging
+    const pc::PageDesc d{nullptr, nullptr, vaddr0, pid0};
+    int rc = launch_crypt(key->d_words, d, in, out, n, rounds, e->streams[0]);
+    if (rc != PC_OK) return rc;
+    CU(cudaStreamSynchronize(e->streams[0]));
+    return PC_OK;
+  }
   const uint32_t *dkey = nullptr;
   if (raw_key) {
     std::memcpy(e->h_key, raw_key, 32);
@@ -1670,6 +1699,11 @@ int pc_tune(const char *knob, int64_t value) {
     t.kernel = static_cast<int>(value);
     return PC_OK;
   }
+  if (!std::strcmp(knob, "dev_direct")) {
+    if (value < 0 || value > 1) return fail(PC_EINVAL, "dev_direct must be 0 or 1");
+    t.dev_direct = static_cast<int>(value);
+    return PC_OK;
+  }
   if (!std::strcmp(knob, "host_mode")) {
     if (value < 0 || value > 3) return fail(PC_EINVAL, "host_mode must be 0, 1, 2 or 3");
     t.host_mode = static_cast<int>(value);
@@ -1692,6 +1726,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
   else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;
   else if (!std::strcmp(knob, "launches")) *value = static_cast<int64_t>(g_launches.load());
+  else if (!std::strcmp(knob, "dev_direct")) *value = t.dev_direct;
   else if (!std::strcmp(knob, "ctas_per_sm")) *value = t.ctas_per_sm;
   else return fail(PC_EINVAL, "unknown knob '%s'", knob);
   return PC_OK;

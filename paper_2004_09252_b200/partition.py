@@ -15,7 +15,9 @@ Two launch shapes:
   only cross-rank traffic is the benchmark's barrier and max-over-ranks time
   (:func:`max_over_ranks`), never page data;
 * one process, several GPUs: :func:`crypt_pages_multi` drives
-  ``pc_crypt_pages_multi`` (one host thread per device, host-resident pages).
+  ``pc_crypt_pages_multi`` (one host thread per device) over host-resident
+  pages, or over pages resident on one GPU whose ranges the other GPUs pull
+  over NVLink peer-to-peer and return the same way.
 """
 
 from __future__ import annotations
@@ -70,18 +72,40 @@ def max_over_ranks(value: float, device=None) -> float:
 
 
 def crypt_pages_multi(keys: list[DeviceKey], engines: list[Engine], vaddrs, pids,
-                      pages: np.ndarray, out: np.ndarray | None = None, *, rounds: int = 20) -> np.ndarray:
-    """Host-resident batch split by contiguous page range over len(engines)
-    devices (keys[g] must live on engines[g]'s device)."""
+                      pages, out=None, *, rounds: int = 20):
+    """A batch split by contiguous page range over len(engines) devices
+    (keys[g] must live on engines[g]'s device), no collective.
+
+    ``pages`` is host memory (numpy / buffer: PCIe to every GPU), or a CUDA
+    tensor resident on one GPU: that GPU ciphers its own range in place and
+    every other range crosses NVLink peer-to-peer to its GPU and back
+    (SURVEY §8e).  vaddrs/pids: int or host arrays.  Synchronous."""
     if len(keys) != len(engines) or not engines:
         raise ContractViolation("need one key per engine")
     for k, e in zip(keys, engines):
         if k.device != e.device:
             raise ContractViolation(f"key on device {k.device}, engine on {e.device}")
-    arr = np.ascontiguousarray(pages, dtype=np.uint8).reshape(-1, PAGE_SIZE)
-    n = arr.shape[0]
-    if out is None:
-        out = np.empty_like(arr)
+    if type(pages).__module__.startswith("torch") and pages.is_cuda:
+        import torch
+
+        if pages.dtype != torch.uint8 or not pages.is_contiguous() or pages.numel() % PAGE_SIZE:
+            raise ContractViolation("device pages must be a contiguous uint8 tensor of whole pages")
+        n = pages.numel() // PAGE_SIZE
+        if out is None:
+            out = torch.empty_like(pages)
+        elif not (out.is_cuda and out.dtype == torch.uint8 and out.is_contiguous() and out.numel() == pages.numel()):
+            raise ContractViolation("out must be a contiguous uint8 CUDA tensor like pages")
+        # the library's streams must see the producer's writes
+        torch.cuda.current_stream(pages.device).synchronize()
+        if out.device != pages.device:
+            torch.cuda.current_stream(out.device).synchronize()
+        src, dst = pages.data_ptr(), out.data_ptr()
+    else:
+        arr = np.ascontiguousarray(pages, dtype=np.uint8).reshape(-1, PAGE_SIZE)
+        n = arr.shape[0]
+        if out is None:
+            out = np.empty_like(arr)
+        src, dst = arr.ctypes.data, out.ctypes.data
     v_arr, vaddr0 = _host_vaddrs(vaddrs, n)
     p_arr, pid0 = _host_pids(pids, n)
     G = len(engines)
@@ -90,5 +114,5 @@ def crypt_pages_multi(keys: list[DeviceKey], engines: list[Engine], vaddrs, pids
     _native.call("pc_crypt_pages_multi", eh, kh, G,
                  None if v_arr is None else v_arr.ctypes.data,
                  None if p_arr is None else p_arr.ctypes.data,
-                 vaddr0, pid0, arr.ctypes.data, out.ctypes.data, n, rounds)
+                 vaddr0, pid0, src, dst, n, rounds)
     return out

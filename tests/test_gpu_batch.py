@@ -295,3 +295,38 @@ class TestMultiDevice:
                 k.destroy()
             for e in engines:
                 e.destroy()
+
+    @pytest.mark.parametrize("dev_direct", [1, 0])
+    def test_device_resident_partition(self, cuda, dev_direct, knob):
+        """Pages resident on one GPU, split over engines: the
+        owning GPU runs in place, the others pull their range peer-to-peer.
+        With one GPU, dev_direct=0 forces every range through the engines'
+        staging ring (the peer path, as same-device copies)."""
+        import torch
+
+        knob("dev_direct", dev_direct)
+        ndev = torch.cuda.device_count()
+        devs = [d % ndev for d in range(max(3, ndev))]
+        engines = [pc.Engine(d, n_streams=3, chunk_pages=512) for d in devs]
+        keys = [pc.DeviceKey.install(KEY, d) for d in devs]
+        try:
+            host = rand_pages(5003, 17)
+            pages = torch.from_numpy(host).to("cuda:0")
+            want = C.crypt_pages(KEY, None, None, host, vaddr0=BASE, pid0=5, nthreads=8)
+            got = partition.crypt_pages_multi(keys, engines, BASE, 5, pages)
+            assert got.is_cuda and np.array_equal(got.cpu().numpy(), want)
+            # in place, per-page descriptors (staged path), then back
+            va = BASE + 4096 * np.random.default_rng(1).permutation(5003).astype(np.uint64)
+            partition.crypt_pages_multi(keys, engines, va, 5, pages, out=pages)
+            assert np.array_equal(pages.cpu().numpy(), C.crypt_pages(KEY, va, 5, host, nthreads=8))
+            partition.crypt_pages_multi(keys, engines, va, 5, pages, out=pages)
+            assert np.array_equal(pages.cpu().numpy(), host)
+            # through the C ABI directly: device in, host out
+            out = np.empty_like(host)
+            engines[0].crypt_host(keys[0], BASE, 5, pages.data_ptr(), out.ctypes.data, 5003, 20)
+            assert np.array_equal(out, want)
+        finally:
+            for k in keys:
+                k.destroy()
+            for e in engines:
+                e.destroy()
