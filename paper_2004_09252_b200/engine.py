@@ -254,9 +254,12 @@ def _host_vaddrs(vaddrs, n: int):
             raise ContractViolation("contiguous vaddr range overflows u64")
         return None, v0
     if isinstance(vaddrs, (list, tuple, range)):
-        for v in vaddrs:
-            _check_vaddr_int(int(v))
-        vaddrs = np.array([int(v) for v in vaddrs], dtype=np.uint64)
+        ints = [int(v) for v in vaddrs]
+        for v in ints:
+            _check_vaddr_int(v)  # range and alignment: the array needs no more checks
+        if len(ints) != n:
+            raise ContractViolation(f"{len(ints)} vaddrs for {n} pages")
+        return np.array(ints, dtype=np.uint64), 0
     arr = np.asarray(vaddrs)
     if arr.dtype.kind not in "iu":
         raise ContractViolation(f"vaddrs must be integers, got {arr.dtype}")

@@ -60,6 +60,16 @@ class SlidingWindow:
         self._members.add(vaddr)
         return evicted
 
+    def undo_admits(self, admitted: list[int], evicted: list) -> None:
+        """Roll back admit() calls, newest first: admitted[i] evicted
+        evicted[i] (or None)."""
+        for v, e in zip(reversed(admitted), reversed(evicted)):
+            self._queue.pop()
+            self._members.discard(v)
+            if e is not None:
+                self._queue.appendleft(e)
+                self._members.add(e)
+
     def remove(self, vaddr: int) -> bool:
         if vaddr not in self._members:
             return False
@@ -151,10 +161,12 @@ class WindowPager:
         refault_idx = [i for i, v in enumerate(vlist) if self.store.contains(client, v)]
         batch_pos = {v: i for i, v in enumerate(vlist)}
         # window admission in fault order (host state only); collect evictions
-        saved = (deque(win._queue), set(win._members))
+        # and keep an undo log (admission i evicted undo[i] or None)
+        undo: list = []
         evicted: list[int] = []
         for v in vlist:
             e = win.admit(v)
+            undo.append(e)
             if e is not None:
                 evicted.append(e)
         try:
@@ -187,7 +199,7 @@ class WindowPager:
                     got.fill(0)
                     m.gpu_batches += 1
         except BaseException:
-            win._queue, win._members = saved
+            win.undo_admits(vlist, undo)
             raise
         m.decrypt_ops += len(refault_idx)
         m.first_touch_faults += k - len(refault_idx)

@@ -33,7 +33,7 @@ import ctypes
 import numpy as np
 
 from . import _native
-from .engine import DeviceKey, Engine, _host_vaddrs, default_engine
+from .engine import DeviceKey, Engine, _addr, _host_vaddrs, default_engine
 from .errors import ContractViolation, PageCryptError
 
 PAGE_SIZE = 4096
@@ -41,6 +41,11 @@ PAGE_SIZE = 4096
 
 class StoreFull(PageCryptError):
     """No free slot left in the device slab."""
+
+
+def _p(arr: np.ndarray):
+    """Address of an array for the C ABI (None when empty)."""
+    return _addr(arr) if arr.size else None
 
 
 def _cid(client) -> int:
@@ -109,7 +114,7 @@ class DevicePageStore:
             raise ContractViolation(f"vaddr {vaddr:#x} not page-aligned")
         arr = self._page(cipher)
         va = np.array([vaddr], dtype=np.uint64)
-        self._call("pc_store_put", self._h, _cid(client), client.pid, va.ctypes.data, 1, arr.ctypes.data, 0)
+        self._call("pc_store_put", self._h, _cid(client), client.pid, _p(va), 1, _p(arr), 0)
 
     def lookup(self, client, vaddr: int):
         """Ciphertext bytes if present, else None (a first touch)."""
@@ -117,13 +122,13 @@ class DevicePageStore:
             return None
         out = np.empty(PAGE_SIZE, dtype=np.uint8)
         va = np.array([vaddr], dtype=np.uint64)
-        self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, 1, out.ctypes.data, 0, 0)
+        self._call("pc_store_get", self._h, _cid(client), client.pid, _p(va), 1, _p(out), 0, 0)
         return out.tobytes()
 
     def remove(self, client, vaddr: int) -> None:
         """Delete an entry; the released slot is wiped before reuse."""
         va = np.array([vaddr], dtype=np.uint64)
-        self._call("pc_store_remove", self._h, _cid(client), va.ctypes.data, 1)
+        self._call("pc_store_remove", self._h, _cid(client), _p(va), 1)
 
     def contains(self, client, vaddr: int) -> bool:
         f = ctypes.c_int()
@@ -139,7 +144,7 @@ class DevicePageStore:
         _native.call("pc_store_list", self._h, _cid(client), None, 0, ctypes.byref(n))
         out = np.empty(n.value, dtype=np.uint64)
         if n.value:
-            _native.call("pc_store_list", self._h, _cid(client), out.ctypes.data, out.size, ctypes.byref(n))
+            _native.call("pc_store_list", self._h, _cid(client), _p(out), out.size, ctypes.byref(n))
         return out
 
     def pages(self, client):
@@ -148,8 +153,8 @@ class DevicePageStore:
         if not va.size:
             return
         out = np.empty((va.size, PAGE_SIZE), dtype=np.uint8)
-        self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
-                   out.ctypes.data, 0, 0)
+        self._call("pc_store_get", self._h, _cid(client), client.pid, _p(va), va.size,
+                   _p(out), 0, 0)
         for v, row in zip(va.tolist(), out):
             yield v, row.tobytes()
 
@@ -179,8 +184,8 @@ class DevicePageStore:
         arr = np.ascontiguousarray(arr, dtype=np.uint8).reshape(-1, PAGE_SIZE)
         if arr.shape[0] != va.size:
             raise ContractViolation(f"{va.size} vaddrs for {arr.shape[0]} pages")
-        self._call("pc_store_put", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
-                   arr.ctypes.data, 1)
+        self._call("pc_store_put", self._h, _cid(client), client.pid, _p(va), va.size,
+                   _p(arr), 1)
 
     def refault_many(self, client, vaddrs, out: np.ndarray | None = None) -> np.ndarray:
         self._need_key()
@@ -189,8 +194,8 @@ class DevicePageStore:
             out = np.empty((va.size, PAGE_SIZE), dtype=np.uint8)
         elif out.nbytes != va.size * PAGE_SIZE or not out.flags.c_contiguous:
             raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
-        self._call("pc_store_get", self._h, _cid(client), client.pid, va.ctypes.data, va.size,
-                   out.ctypes.data, 1, 1)
+        self._call("pc_store_get", self._h, _cid(client), client.pid, _p(va), va.size,
+                   _p(out), 1, 1)
         return out
 
     def swap(self, client, refault_vaddrs, evict_vaddrs, evict_plains, out: np.ndarray | None = None) -> np.ndarray:
@@ -210,6 +215,6 @@ class DevicePageStore:
             out = np.empty((gv.size, PAGE_SIZE), dtype=np.uint8)
         elif out.nbytes != gv.size * PAGE_SIZE or not out.flags.c_contiguous:
             raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
-        self._call("pc_store_swap", self._h, _cid(client), client.pid, gv.ctypes.data, gv.size,
-                   out.ctypes.data, pv.ctypes.data, pv.size, arr.ctypes.data)
+        self._call("pc_store_swap", self._h, _cid(client), client.pid, _p(gv), gv.size,
+                   _p(out), _p(pv), pv.size, _p(arr))
         return out
