@@ -15,6 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
+from .engine import _addr
 
 
 def keystream_words(kw, vaddr, pid, indices, out) -> None:
@@ -32,5 +33,7 @@ def keystream_words(kw, vaddr, pid, indices, out) -> None:
         raise ValueError("kw must hold 8 words")
     if out.dtype != np.uint32 or not out.flags.c_contiguous or out.size != 16 * idx.size:
         raise ValueError("out must be a C-contiguous uint32[16*k] array")
-    _native.call("pc_keystream_words", kw.ctypes.data, int(vaddr) & (2**64 - 1),
-                 int(pid) & 0xFFFFFFFF, idx.ctypes.data, idx.size, out.ctypes.data, 20)
+    if idx.size == 0:
+        return
+    _native.call("pc_keystream_words", _addr(kw), int(vaddr) & (2**64 - 1),
+                 int(pid) & 0xFFFFFFFF, _addr(idx), idx.size, _addr(out), 20)

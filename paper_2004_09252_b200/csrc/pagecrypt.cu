@@ -435,6 +435,23 @@ int keystream_sync(const uint32_t kw[8], const uint32_t *seeds, size_t k, uint32
   // pinned staging: key at [0,32), seeds at [256, 256+16k), keystream after
   std::memcpy(sc.h, kw, 32);
   std::memcpy(sc.h + 256, seeds, 16 * k);
+  if (k <= 4096) {
+    // seam-sized calls (a page is 64 blocks): one zero-copy launch on the
+    // mapped staging -- the kernel reads key and seeds and writes the
+    // keystream across PCIe, no DMA round trips
+    uint8_t *hd = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&hd), sc.h, 0);
+    if (e == cudaSuccess) {
+      rc = launch_keystream(reinterpret_cast<uint32_t *>(hd), reinterpret_cast<uint32_t *>(hd + 256), k,
+                            reinterpret_cast<uint32_t *>(hd + out_off), rounds, sc.st);
+      e = cudaStreamSynchronize(sc.st);
+      if (rc == PC_OK && e == cudaSuccess) std::memcpy(out, sc.h + out_off, 64 * k);
+    }
+    wipe(sc.h, need);
+    if (rc != PC_OK) return rc;
+    CU(e);
+    return PC_OK;
+  }
   uint8_t *d = static_cast<uint8_t *>(sc.d);
   cudaError_t e = cudaMemcpyAsync(d, sc.h, out_off, cudaMemcpyHostToDevice, sc.st);
   if (e == cudaSuccess) {
