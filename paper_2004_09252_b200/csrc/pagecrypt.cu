@@ -109,6 +109,15 @@ struct Tuning {
 std::atomic<uint64_t> g_launches{0};
 inline void counted(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Helper threads for pageable <-> pinned bounce copies (the caller's thread
+// works too): PAGECRYPT_HOST_THREADS, default min(7, cores/2).
+unsigned host_pool_threads() {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int env = env_int("PAGECRYPT_HOST_THREADS", -1);
+  if (env >= 0) return static_cast<unsigned>(std::min(env, 256));
+  return std::min(7u, hw > 1 ? hw / 2 : 0u);
+}
+
 Tuning &tuning() {
   static Tuning t;
   return t;
@@ -875,10 +884,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   if (!pin_in || !pin_out) {
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
-    if (!e->pool) {
-      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-      e->pool.reset(new pc::HostPool(std::min(7u, hw > 1 ? hw / 2 : 0u)));
-    }
+    if (!e->pool) e->pool.reset(new pc::HostPool(host_pool_threads()));
   }
   // Chunk schedule: ramp up C/8, C/4, C/2 at the start and down at the end
   // (when the batch is large enough) so the pipeline fills and drains with
@@ -1101,10 +1107,7 @@ extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, siz
   if (!pinned) {
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
-    if (!e->pool) {
-      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-      e->pool.reset(new pc::HostPool(std::min(7u, hw > 1 ? hw / 2 : 0u)));
-    }
+    if (!e->pool) e->pool.reset(new pc::HostPool(host_pool_threads()));
   }
   auto *hb = static_cast<uint8_t *>(host);
   const size_t n_chunks = (n + C - 1) / C;
