@@ -1,3 +1,6 @@
+"""Diagnostic: the worker service running beside bulk kernels, keys, engines
+and the HBM store in one process (with TORCH_FIRST=1: torch initialised
+before the service), under a 20 s faulthandler deadline."""
 import faulthandler, sys, os, time, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 faulthandler.dump_traceback_later(20, exit=True)

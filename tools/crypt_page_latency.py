@@ -1,3 +1,5 @@
+"""p50/p99 latency of the reference-API crypt_page for each key/page type
+(bytes, MasterKey + bytearray, ndarray, DeviceKey)."""
 import time, os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np

@@ -1,3 +1,5 @@
+"""Diagnostic: host-resident pinned batches of 1/4/16 GiB, out of place vs in
+place, through crypt_pages and crypt_pages_multi (one engine)."""
 import sys, os, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -1,3 +1,6 @@
+"""Diagnostic: ChaCha12 kernel time vs SM/memory clocks, power and clock-event
+reasons (NVML) over back-to-back launches -- the power-cap study behind
+profiles/r01_clock_power_sweep.txt."""
 import sys, os, time, json
 sys.path.insert(0, os.getcwd())
 import torch

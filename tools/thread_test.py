@@ -1,3 +1,6 @@
+"""Diagnostic: pc_crypt_pages_host on 1 GiB pinned from the main thread, from a
+fresh Python thread and through pc_crypt_pages_multi (the per-engine runner
+thread) -- the first-CUDA-call-per-thread cost noted in DESIGN.md §6."""
 import sys, os, time, json, threading, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
