@@ -102,8 +102,10 @@ int pc_crypt_pages_dev(const pc_key *key, const uint64_t *vaddrs, const uint32_t
  * ring on several CUDA streams so H2D, cipher and D2H overlap; small
  * batches take a single-launch path.  in/out may also be device memory of
  * any GPU: pages on the engine's own GPU (contiguous vaddrs, scalar pid,
- * DeviceKey) run as one in-place launch; pages on another GPU stream through
- * the engine's ring by peer copies (NVLink) instead of PCIe.  vaddrs/pids: host arrays or NULL.
+ * DeviceKey) run as one in-place launch; pages on another GPU are ciphered in
+ * place by this GPU's kernel over NVLink when peer access is available (same
+ * conditions; knob "peer_direct"), else stream through the engine's ring by
+ * peer copies.  vaddrs/pids: host arrays or NULL.
  * Synchronous: returns when out holds the result.  `key` may be NULL when
  * raw_key is given (caller-key mode: the engine copies raw_key into a device
  * slot for this call and zeroes it before returning). */
@@ -231,7 +233,8 @@ int pc_intpeak(int device, int kind, double *ops_per_s);
 /* Process-wide knobs: "rotmask" (compiled FMA-pipe rotate pattern of the
  * crypt kernel, see chacha.cuh), "small_mode" (0 staged copies / 1 zero-copy
  * for small host batches), "small_max", "kernel" (0 auto, 1..5 page-kernel
- * variant), "host_mode" (0..3 host pipeline), "ctas_per_sm"; pc_tune_get
+ * variant), "host_mode" (0..3 host pipeline), "ctas_per_sm", "dev_direct",
+ * "peer_direct" (device-memory endpoints, see (v)); pc_tune_get
  * also reads "launches", the number of kernels this library has launched. */
 int pc_tune(const char *knob, int64_t value);
 int pc_tune_get(const char *knob, int64_t *value);

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <string>
@@ -94,6 +95,8 @@ struct Tuning {
   std::atomic<int> ctas_per_sm{0};     // k_crypt_pages residency; 0 = occupancy calculator
   std::atomic<int> dev_direct{1};      // device pages on the engine's own GPU: 1 = one in-place launch,
                                        // 0 = stage through the engine's slots (tests the peer path on 1 GPU)
+  std::atomic<int> peer_direct{1};     // device pages on a peer GPU: 1 = kernel works on them in place over
+                                       // NVLink when peer access is available, 0 = peer copies via staging
   Tuning() {
     kernel = env_int("PAGECRYPT_KERNEL", 0);
     host_mode = env_int("PAGECRYPT_HOST_MODE", 2);
@@ -357,6 +360,32 @@ bool device_memory(const void *p, int *device) {
   if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return false;
   *device = a.device;
   return true;
+}
+
+// Can kernels on `dev` load/store `peer`'s memory?  Enables peer access once
+// per (dev, peer) pair and caches the answer (NVSwitch: every pair can).
+bool peer_access(int dev, int peer) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, bool> known;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = known.find({dev, peer});
+  if (it != known.end()) return it->second;
+  int can = 0;
+  bool ok = cudaDeviceCanAccessPeer(&can, dev, peer) == cudaSuccess && can;
+  if (ok) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+    ok = e == cudaSuccess;
+    cudaGetLastError(); // clear a sticky-free error from the enable call
+    cudaSetDevice(cur);
+  } else {
+    cudaGetLastError();
+  }
+  known[{dev, peer}] = ok;
+  return ok;
 }
 
 // Process-wide recycler of pinned host buffers.  cudaFreeHost (like cudaFree
@@ -1010,6 +1039,18 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
     // pages already in this GPU's memory: one in-place launch, no staging
     const pc::PageDesc d{nullptr, nullptr, vaddr0, pid0};
     int rc = launch_crypt(key->d_words, d, in, out, n, rounds, e->streams[0]);
+    if (rc != PC_OK) return rc;
+    CU(cudaStreamSynchronize(e->streams[0]));
+    return PC_OK;
+  }
+  if (din && dout && gin == gout && gin != e->device && !vaddrs && !pids && !raw_key &&
+      tuning().peer_direct.load() && peer_access(e->device, gin)) {
+    // pages in a peer GPU's memory (NVLink/NVSwitch): this GPU's kernel reads
+    // and writes them in place over the fabric -- the scatter, the cipher and
+    // the gather are one kernel, with no staging copies.  The coalesced
+    // variant keeps every warp access a 512-byte contiguous run.
+    const pc::PageDesc d{nullptr, nullptr, vaddr0, pid0};
+    int rc = launch_crypt(key->d_words, d, in, out, n, rounds, e->streams[0], 3);
     if (rc != PC_OK) return rc;
     CU(cudaStreamSynchronize(e->streams[0]));
     return PC_OK;
@@ -1719,6 +1760,11 @@ int pc_tune(const char *knob, int64_t value) {
     t.kernel = static_cast<int>(value);
     return PC_OK;
   }
+  if (!std::strcmp(knob, "peer_direct")) {
+    if (value < 0 || value > 1) return fail(PC_EINVAL, "peer_direct must be 0 or 1");
+    t.peer_direct = static_cast<int>(value);
+    return PC_OK;
+  }
   if (!std::strcmp(knob, "dev_direct")) {
     if (value < 0 || value > 1) return fail(PC_EINVAL, "dev_direct must be 0 or 1");
     t.dev_direct = static_cast<int>(value);
@@ -1747,6 +1793,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;
   else if (!std::strcmp(knob, "launches")) *value = static_cast<int64_t>(g_launches.load());
   else if (!std::strcmp(knob, "dev_direct")) *value = t.dev_direct;
+  else if (!std::strcmp(knob, "peer_direct")) *value = t.peer_direct;
   else if (!std::strcmp(knob, "ctas_per_sm")) *value = t.ctas_per_sm;
   else return fail(PC_EINVAL, "unknown knob '%s'", knob);
   return PC_OK;
