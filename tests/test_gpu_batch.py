@@ -182,6 +182,32 @@ class TestFullSize:
         del pages, ct, back
         torch.cuda.empty_cache()
 
+    @pytest.mark.parametrize("rounds", [8, 12, 20])
+    def test_1gib_every_byte_against_the_oracle(self, dkey, rounds):
+        """The whole BASELINE configs[1]/[2] batch (1 GiB, the bench's
+        workload: contiguous vaddrs from BASE, pid 1) byte-exact against the
+        C oracle on all host cores, per-page descriptors included."""
+        import os
+
+        import torch
+
+        n = 262_144
+        host = np.random.default_rng(rounds).integers(0, 256, size=(n, 4096), dtype=np.uint8)
+        pages = torch.from_numpy(host).cuda()
+        threads = max(1, len(os.sched_getaffinity(0)))
+        got = pc.crypt_pages(dkey, BASE, 1, pages, rounds=rounds).cpu().numpy()
+        want = C.crypt_pages(KEY, None, None, host, rounds=rounds, vaddr0=BASE, pid0=1, nthreads=threads)
+        assert np.array_equal(got, want)
+        # per-page descriptors: a permutation of vaddrs, 64 pids
+        va = BASE + 4096 * np.random.default_rng(7).permutation(n).astype(np.uint64)
+        pid = (1 + np.arange(n) % 64).astype(np.uint32)
+        got = pc.crypt_pages(dkey, torch.from_numpy(va.view(np.int64)).cuda(),
+                             torch.from_numpy(pid.view(np.int32)).cuda(), pages, rounds=rounds).cpu().numpy()
+        want = C.crypt_pages(KEY, va, pid, host, rounds=rounds, nthreads=threads)
+        assert np.array_equal(got, want)
+        del pages
+        torch.cuda.empty_cache()
+
 
 class TestHostPath:
     @pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 2048, 2049, 10_000])
