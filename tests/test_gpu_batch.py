@@ -208,6 +208,24 @@ class TestFullSize:
         del pages
         torch.cuda.empty_cache()
 
+    def test_1gib_host_resident_every_byte(self, dkey):
+        """The bench's e2e leg (1 GiB pinned host pages through the ramped
+        H2D / cipher / D2H pipeline, out of place and in place) byte-exact."""
+        import os
+
+        import torch
+
+        n = 262_144
+        host = np.random.default_rng(5).integers(0, 256, size=(n, 4096), dtype=np.uint8)
+        threads = max(1, len(os.sched_getaffinity(0)))
+        want = C.crypt_pages(KEY, None, None, host, vaddr0=BASE, pid0=1, nthreads=threads)
+        src = torch.from_numpy(host).pin_memory()
+        dst = torch.empty_like(src).pin_memory()
+        pc.crypt_pages(dkey, BASE, 1, src, out=dst)
+        assert np.array_equal(dst.numpy(), want)
+        pc.crypt_pages(dkey, BASE, 1, src, out=src)
+        assert np.array_equal(src.numpy(), want)
+
 
 class TestHostPath:
     @pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 2048, 2049, 10_000])
