@@ -87,3 +87,33 @@ def test_no_kernel_uses_local_memory():
         assert k in names
     bad = [(f, st, lo) for f, _, st, lo in fns if st != "0" or lo != "0"]
     assert not bad
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/pagecrypt.h is a C ABI: a C99 program (-pedantic -Werror)
+    includes it, links libpagecrypt.so and calls it -- no C++ or torch types
+    anywhere on the boundary."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    _native.load()  # builds must exist
+    src = tmp_path / "abi.c"
+    src.write_text(
+        '#include "pagecrypt.h"\n#include <stdio.h>\n'
+        "int main(void) {\n"
+        "  int n = -1;\n"
+        "  if (pc_abi_version() != PC_ABI_VERSION) return 2;\n"
+        "  (void)pc_device_count(&n);\n"
+        "  if (pc_keystream_words(0, 0, 0, 0, 1, 0, 20) != PC_EINVAL) return 3;\n"
+        '  printf("%s\\n", pc_last_error());\n'
+        "  return 0;\n}\n")
+    exe = tmp_path / "abi"
+    libdir = os.path.dirname(_native.LIB_PATH)
+    subprocess.run([gcc, "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-L", libdir, "-lpagecrypt", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "NULL" in r.stdout
