@@ -144,6 +144,8 @@ class WindowPager:
     def fault_batch(self, client, vaddrs) -> np.ndarray:
         """Resolve faults on distinct, non-resident pages, in order; returns
         their plaintexts as uint8[k, 4096]."""
+        if len(vaddrs) == 1:
+            return self._fault_one(client, vaddrs[0])
         win = self._window(client)
         m = self.metrics[client]
         vlist = [int(v) for v in vaddrs]
@@ -206,6 +208,49 @@ class WindowPager:
         m.faults += k
         m.evictions += len(evicted)
         m.encrypt_ops += len(evicted)
+        return out
+
+    def _fault_one(self, client, vaddr) -> np.ndarray:
+        """fault_batch for one page (the reference's flow): the same steps
+        without the batch bookkeeping.  The page it evicts (if any) was
+        resident before, so a refault and its eviction are one swap."""
+        win = self._window(client)
+        m = self.metrics[client]
+        v = int(vaddr)
+        if v % PAGE_SIZE:
+            raise ContractViolation(f"vaddr {v:#x} not page-aligned")
+        if win.resident(v):
+            raise ContractViolation(f"fault on resident page {v:#x}")
+        refault = self.store.contains(client, v)
+        e = win.admit(v)
+        try:
+            if refault and e is not None:
+                plain_ev = self._from_client(client, [e])
+                out = self.store.swap(client, [v], [e], plain_ev)
+                plain_ev.fill(0)  # scratch_evict.wipe(), orchestrator.py:239
+                m.gpu_batches += 1
+            else:
+                if refault:
+                    out = self.store.refault_many(client, [v])
+                    m.gpu_batches += 1
+                else:
+                    out = np.zeros((1, PAGE_SIZE), dtype=np.uint8)  # first touch
+                if e is not None:
+                    plain_ev = self._from_client(client, [e])
+                    self.store.evict_many(client, [e], plain_ev)
+                    plain_ev.fill(0)
+                    m.gpu_batches += 1
+        except BaseException:
+            win.undo_admits([v], [e])
+            raise
+        m.faults += 1
+        if refault:
+            m.decrypt_ops += 1
+        else:
+            m.first_touch_faults += 1
+        if e is not None:
+            m.evictions += 1
+            m.encrypt_ops += 1
         return out
 
     def _from_client(self, client, vaddrs: list[int]) -> np.ndarray:
