@@ -374,3 +374,67 @@ class TestMultiDevice:
                 k.destroy()
             for e in engines:
                 e.destroy()
+
+
+class TestConcurrentCallers:
+    """The reference cipher is 'pure and safe for concurrent callers'
+    (SPEC.md:101-102).  Eight host threads share the default engine, one
+    HBM store and the keystream seams, each checking every result against
+    the oracle."""
+
+    def test_threads_share_engine_store_and_seams(self, dkey, cuda):
+        import threading
+
+        import torch
+
+        from paper_2004_09252_b200 import _chacha_cuda
+        from paper_2004_09252_b200.store import DevicePageStore
+        from paper_2004_09252_b200.workers import ClientId
+
+        store = DevicePageStore(4096, dkey)
+        errors = []
+
+        def worker(t):
+            try:
+                rng = np.random.default_rng(100 + t)
+                cl = ClientId(500 + t, 0)
+                stream = torch.cuda.Stream()
+                for it in range(6):
+                    n = int(rng.integers(1, 3000))
+                    pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
+                    v0 = BASE + 4096 * int(rng.integers(0, 1 << 20))
+                    want = C.crypt_pages(KEY, None, None, pages, vaddr0=v0, pid0=cl.pid, nthreads=2)
+                    # host batch through the shared default engine (pageable and pinned)
+                    got = pc.crypt_pages(dkey, v0, cl.pid, pages)
+                    assert np.array_equal(got, want)
+                    src = torch.from_numpy(pages).pin_memory()
+                    dst = pc.crypt_pages(dkey, v0, cl.pid, src)
+                    assert np.array_equal(dst.numpy(), want)
+                    # device batch on this thread's own stream
+                    with torch.cuda.stream(stream):
+                        d = pc.crypt_pages(dkey, v0, cl.pid, torch.from_numpy(pages).cuda(), stream=stream)
+                    stream.synchronize()
+                    assert np.array_equal(d.cpu().numpy(), want)
+                    # reference single-page API with raw key bytes, and the kernel seam
+                    assert pc.crypt_page(KEY, v0, cl.pid, pages[0].tobytes()) == want[0].tobytes()
+                    out = np.empty(1024, np.uint32)
+                    _chacha_cuda.keystream_words(np.frombuffer(KEY, "<u4"), np.uint64(v0), np.uint32(cl.pid),
+                                                 np.arange(64, dtype=np.int64), out)
+                    assert out.tobytes() == (want[0] ^ pages[0]).tobytes()
+                    # the shared HBM store: evict then refault this thread's pages
+                    m = min(n, 200)
+                    va = [v0 + 4096 * i for i in range(m)]
+                    store.evict_many(cl, va, pages[:m])
+                    assert store.lookup(cl, va[0]) == want[0].tobytes()
+                    assert np.array_equal(store.refault_many(cl, va), pages[:m])
+            except BaseException as exc:  # surfaced below
+                errors.append((t, repr(exc)))
+
+        threads = [threading.Thread(target=worker, args=(t,)) for t in range(8)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        assert not errors, errors
+        assert store.free_slots == 4096
+        store.close()
