@@ -248,3 +248,28 @@ def test_swap_is_all_or_nothing(dkey):
     assert s.contains(C1, 0x1000) and s.contains(C1, 0x2000) and not s.contains(C1, 0x3000)
     assert s.free_slots == 14
     assert s.refault(C1, 0x1000) == page(1)
+
+
+def test_batch_naming_a_page_twice_is_rejected_whole(dkey):
+    """remove / refault batches that name a page twice fail without freeing
+    any slot (a double free would hand one slot to two pages later)."""
+    import ctypes
+
+    from paper_2004_09252_b200 import _native
+    from paper_2004_09252_b200.store import _cid
+
+    s = DevicePageStore(8, dkey)
+    s.evict_many(C1, [0x1000, 0x2000], np.stack([np.frombuffer(page(1), np.uint8), np.frombuffer(page(2), np.uint8)]))
+    lib = _native.load()
+    va = np.array([0x1000, 0x2000, 0x1000], dtype=np.uint64)
+    assert lib.pc_store_remove(s._h, _cid(C1), va.ctypes.data, 3) == _native.PC_EINVAL
+    assert b"duplicate" in lib.pc_last_error()
+    assert s.free_slots == 6 and s.contains(C1, 0x1000) and s.contains(C1, 0x2000)
+    with pytest.raises(ContractViolation):
+        s.refault_many(C1, [0x2000, 0x1000, 0x2000])
+    assert s.free_slots == 6
+    assert s.refault(C1, 0x1000) == page(1) and s.refault(C1, 0x2000) == page(2)
+    assert s.free_slots == 8
+    # duplicate lookups (no remove) are fine
+    s.evict(C1, 0x3000, page(3))
+    assert s.lookup(C1, 0x3000) == s.lookup(C1, 0x3000)
