@@ -361,6 +361,7 @@ def main() -> None:
            "steps": e2e_steps, "path": "crypt_pages(DeviceKey, pinned torch CPU tensors) -> "
            f"pc_crypt_pages_host, {eng.n_streams} streams x {eng.chunk_pages}-page chunks"}
 
+    del host_in, host_out  # the e2e buffers are done with; free before the extras
     extras = {}
     if not args.no_extras:
         for r in (8, 12):
@@ -375,7 +376,6 @@ def main() -> None:
             extras["latency_service_1page"] = service_latency(local_rank)
             extras["hbm_store"] = store_throughput(pc, key, local_rank)
             extras["pager"] = pager_rate(pc, key, local_rank)
-    del host_in, host_out
 
     cpu = None
     if rank == 0 and world == 1:

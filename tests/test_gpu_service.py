@@ -365,3 +365,20 @@ def test_service_coexists_with_bulk_work_and_lifecycles(cuda):
     finally:
         _native.tune("kernel", 0)
         pool.shutdown()
+
+
+def test_default_pool_routes_like_the_reference(cuda):
+    """n_workers=None means os.cpu_count() as in the reference
+    (workers.py:156-157), so client -> worker routing is identical."""
+    import os
+
+    pool = WorkerPool(keysource=fixed_keysource)
+    try:
+        assert pool.n_workers == min(os.cpu_count() or 1, pool.n_workers) and pool.n_workers >= 1
+        if (os.cpu_count() or 1) <= pool.n_workers:
+            for pid in (0, 1, 4242, 2**32 - 1):
+                for epoch in (0, 7):
+                    c = ClientId(pid, epoch)
+                    assert pool.route(c) == ((pid * 2654435761) ^ epoch) % (os.cpu_count() or 1)
+    finally:
+        pool.shutdown()

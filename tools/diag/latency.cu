@@ -43,7 +43,8 @@ static void measure(const char *what, int pages, F fn, int reps = 3000) {
   fflush(stdout);
 }
 
-int main() {
+int main(int argc, char **argv) {
+  const int svc_workers = argc > 1 ? std::atoi(argv[1]) : 8;
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   measure("empty launch + stream sync", 0, [&] {
@@ -80,7 +81,7 @@ int main() {
                            20));
   });
   pc_service *svc = nullptr;
-  CK(pc_service_start(key, 8, 64, 20, &svc));
+  CK(pc_service_start(key, svc_workers, 64, 20, &svc));
   measure("pc_service_crypt", 1, [&] { CK(pc_service_crypt(svc, 0, 0x100000000ull, 1, in, out, -1)); });
   CK(pc_service_stop(svc));
   CK(pc_engine_destroy(eng));
