@@ -71,6 +71,18 @@ class Completion:
         self.error = error
         self._done = pool is None
 
+    def signal(self, error=None) -> None:
+        """Mark the request finished, optionally with an error that ``wait``
+        re-raises (workers.py:38-42).  The GPU service completes requests by
+        itself; signalling a request it still holds first waits for the GPU to
+        let go of the page, so no result can land in a released buffer."""
+        if not self._done:
+            rc = self._pool._lib.pc_service_wait(self._pool._svc, self._worker, self._ticket, -1)
+            _native.check(rc)
+            self._done = True
+            self._pool._pending.pop((self._worker, self._ticket), None)
+        self.error = error
+
     def wait(self, timeout: float | None = None) -> None:
         if not self._done:
             us = -1 if timeout is None else int(timeout * 1e6)

@@ -382,3 +382,22 @@ def test_default_pool_routes_like_the_reference(cuda):
                     assert pool.route(c) == ((pid * 2654435761) ^ epoch) % (os.cpu_count() or 1)
     finally:
         pool.shutdown()
+
+
+def test_completion_signal_after_gpu_release(cuda):
+    """Completion.signal (workers.py:38-42) on a request the GPU still holds
+    waits for it first; the recorded error is what wait() raises."""
+    pool = make_pool(2)
+    try:
+        page = bytearray(4096)
+        c = pool.submit(ClientId(1, 0), 0x1000, "encrypt", page)
+        c.signal(PoolError("cancelled by caller"))
+        assert c.done
+        with pytest.raises(PoolError, match="cancelled"):
+            c.wait()
+        assert bytes(page) == O.crypt_page(KEY, 0x1000, 1, bytes(4096))
+        ok = Completion()
+        ok.signal()
+        ok.wait()
+    finally:
+        pool.shutdown()
