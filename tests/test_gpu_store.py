@@ -273,3 +273,22 @@ def test_batch_naming_a_page_twice_is_rejected_whole(dkey):
     # duplicate lookups (no remove) are fine
     s.evict(C1, 0x3000, page(3))
     assert s.lookup(C1, 0x3000) == s.lookup(C1, 0x3000)
+
+
+def test_stored_ciphertext_histogram(dkey):
+    """The reference's ciphertext smoke test (analyzer.ciphertext_histogram_ok,
+    pkg/tests/test_analyzer.py:200-215): 260 low-entropy pages (each one
+    repeated byte) evicted into the HBM store, >= 1 MiB of ciphertext, and no
+    byte value more frequent than 3x uniform -- here also a chi-square bound."""
+    s = DevicePageStore(512, dkey)
+    pages = np.stack([np.full(4096, i % 256, np.uint8) for i in range(260)])
+    va = [0x1_0000_0000 + 4096 * i for i in range(260)]
+    s.evict_many(ClientId(5, 0), va, pages)
+    blob = np.concatenate([np.frombuffer(ct, np.uint8) for _, ct in s.pages(ClientId(5, 0))])
+    assert blob.size >= 1 << 20
+    counts = np.bincount(blob, minlength=256)
+    expect = blob.size / 256
+    assert counts.max() <= 3.0 * expect
+    chi2 = float(((counts - expect) ** 2 / expect).sum())
+    assert chi2 < 400  # 255 dof: mean 255, sd ~22.6
+    s.close()
