@@ -192,3 +192,46 @@ def test_contract_errors_on_cpu():
     pager.fault(C, 0x1000)
     with pytest.raises(ContractViolation):
         pager.fault(C, 0x1000)
+
+
+def test_clients_are_isolated():
+    """Several clients interleave faults through one pager and one store:
+    each sees exactly its own single-client history (test_bench.py:143-156
+    counter isolation; the pid enters every ciphertext)."""
+    W = 3
+    store = FakeStore()
+    mems = {}
+
+    def fetch(client, vaddrs):
+        return np.stack([np.frombuffer(mems[client].pop(v), np.uint8) for v in vaddrs])
+
+    pager = WindowPager(store, fetch, window_capacity=W)
+    clients = [ClientId(10 + i, i) for i in range(3)]
+    solo = {}
+    for cl in clients:
+        pager.register(cl)
+        mems[cl] = {}
+        # the same client alone, for reference
+        s_store = FakeStore()
+        s_mem = {}
+        s_pager = WindowPager(s_store, lambda c, vs, m=s_mem: np.stack([np.frombuffer(m.pop(v), np.uint8) for v in vs]), W)
+        s_pager.register(cl)
+        solo[cl] = (s_pager, s_store, s_mem)
+    rng = random.Random(5)
+    pages = [0x70000 + 4096 * i for i in range(8)]
+    for _ in range(150):
+        cl = rng.choice(clients)
+        v = rng.choice([p for p in pages if p not in pager.window(cl)])
+        got = pager.fault(cl, v)
+        s_pager, s_store, s_mem = solo[cl]
+        want = s_pager.fault(cl, v)
+        assert got == want
+        data = scribble(v ^ cl.pid, got)
+        mems[cl][v] = data
+        s_mem[v] = data
+    for cl in clients:
+        s_pager, s_store, _ = solo[cl]
+        assert pager.window(cl) == s_pager.window(cl)
+        assert {k: c for k, c in store.ct.items() if k[0] == cl} == s_store.ct
+        a, b = pager.metrics[cl], s_pager.metrics[cl]
+        assert (a.faults, a.evictions, a.decrypt_ops, a.encrypt_ops) == (b.faults, b.evictions, b.decrypt_ops, b.encrypt_ops)
