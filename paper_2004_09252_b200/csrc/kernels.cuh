@@ -45,6 +45,13 @@ __device__ __forceinline__ void load_key(const uint32_t *__restrict__ key, uint3
   k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
 }
 
+// A page's descriptor (vaddr, pid): loaded one page ahead by the persistent
+// kernels so the global-load latency hides under the current page's rounds.
+__device__ __forceinline__ void desc_fetch(const PageDesc &d, uint64_t page, uint64_t &va, uint32_t &pid) {
+  va = d.vaddrs ? __ldg(d.vaddrs + page) : d.vaddr0 + (page << 12);
+  pid = d.pids ? __ldg(d.pids + page) : d.pid0;
+}
+
 __device__ __forceinline__ void page_seed(const PageDesc &d, uint64_t page, uint32_t (&s)[4]) {
   const uint64_t va = d.vaddrs ? __ldg(d.vaddrs + page) : d.vaddr0 + (page << 12);
   s[0] = static_cast<uint32_t>(va);        // word 12 = vaddr lo
@@ -197,17 +204,24 @@ k_crypt_pages_coalesced(const uint32_t *__restrict__ key, PageDesc desc, const u
   // coalesced: lane l of load j takes tile chunk q = 32j + l
   const uint4 *src = in + page * 256 + half * 128 + lane;
   uint4 d0 = ld_v4(src), d1 = ld_v4(src + 32), d2 = ld_v4(src + 64), d3 = ld_v4(src + 96);
+  uint64_t nva;
+  uint32_t npid;
+  desc_fetch(desc, page, nva, npid);
   for (;;) {
     const uint64_t next = page + stride;
     const bool has_next = next < n_pages;
-    // stage this half page into shared memory (swizzled), then prefetch the next
+    // stage this half page into shared memory (swizzled), then prefetch the
+    // next page and its descriptor
     t[swz(lane)] = d0; t[swz(lane + 32)] = d1; t[swz(lane + 64)] = d2; t[swz(lane + 96)] = d3;
+    uint32_t s[4];
+    s[0] = static_cast<uint32_t>(nva);
+    s[1] = static_cast<uint32_t>(nva >> 32);
+    s[2] = npid;
     if (has_next) {
       const uint4 *ns = in + next * 256 + half * 128 + lane;
       d0 = ld_v4(ns); d1 = ld_v4(ns + 32); d2 = ld_v4(ns + 64); d3 = ld_v4(ns + 96);
+      desc_fetch(desc, next, nva, npid);
     }
-    uint32_t s[4];
-    page_seed(desc, page, s);
     if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
       c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
       quarter_round<0>(c1a, c1b, c1c, c1d, rm);
@@ -441,6 +455,9 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = desc.pid0;
     quarter_round<0>(c2a, c2b, c2c, c2d, rm);
   }
+  uint64_t nva = 0;
+  uint32_t npid = 0;
+  if constexpr (!CONTIG) desc_fetch(desc, page, nva, npid);
   int st = 0;
   for (;;) {
     issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
@@ -456,9 +473,11 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
         cached = true;
       }
     } else {
-      uint32_t sd[4];
-      page_seed(desc, page, sd);
-      s[0] = sd[0]; s[1] = sd[1]; s[2] = sd[2];
+      // this page's descriptor was fetched one page ago; fetch the next one
+      s[0] = static_cast<uint32_t>(nva);
+      s[1] = static_cast<uint32_t>(nva >> 32);
+      s[2] = npid;
+      if (page + stride < n_pages) desc_fetch(desc, page + stride, nva, npid);
       if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
         c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
         quarter_round<0>(c1a, c1b, c1c, c1d, rm);
