@@ -411,10 +411,16 @@ __device__ __forceinline__ void cp_async_wait() {
 // column round is hoisted out of the loop entirely; the general case reads
 // per-page descriptors.  Page counts are < 2^31 (the host splits larger
 // batches).
-template <int ROUNDS, bool CONTIG>
+//
+// DM (descriptor mode) compiles each descriptor shape separately: bit 0 = a
+// per-page vaddr array, bit 1 = a per-page pid array, so no loop carries a
+// null-pointer test and a scalar pid keeps its column round hoisted.
+template <int ROUNDS, int DM>
 __global__ void __launch_bounds__(256, 4)
 k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
                     uint32_t n_pages) {
+  constexpr bool CONTIG = DM == 0;
+  constexpr bool VA = (DM & 1) != 0, PA = (DM & 2) != 0;
   constexpr RotMul rm{};
   constexpr int kStages = 3;
   __shared__ uint4 ring[kStages][256 * 4]; // 16 KiB per stage
@@ -451,41 +457,43 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
   bool cached = false;
   uint64_t va = desc.vaddr0 + (static_cast<uint64_t>(page) << 12);
   const uint64_t va_step = static_cast<uint64_t>(stride) << 12;
-  if constexpr (CONTIG) {
+  if constexpr (!PA) {
     c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = desc.pid0;
     quarter_round<0>(c2a, c2b, c2c, c2d, rm);
   }
+  // per-page descriptors are loaded one page ahead, so the load latency
+  // hides under the current page's rounds
   uint64_t nva = 0;
   uint32_t npid = 0;
-  if constexpr (!CONTIG) desc_fetch(desc, page, nva, npid);
+  if constexpr (VA) nva = __ldg(desc.vaddrs + page);
+  if constexpr (PA) npid = __ldg(desc.pids + page);
+  bool pid_cached = false;
   int st = 0;
   for (;;) {
     issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
     uint32_t s[3];
-    if constexpr (CONTIG) {
-      s[0] = static_cast<uint32_t>(va);
-      s[1] = static_cast<uint32_t>(va >> 32);
-      s[2] = desc.pid0;
-      if (!cached || s[1] != cached_hi) {
-        c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
-        quarter_round<0>(c1a, c1b, c1c, c1d, rm);
-        cached_hi = s[1];
-        cached = true;
+    const uint64_t v = VA ? nva : va;
+    s[0] = static_cast<uint32_t>(v);
+    s[1] = static_cast<uint32_t>(v >> 32);
+    s[2] = PA ? npid : desc.pid0;
+    if constexpr (!CONTIG) {
+      if (page + stride < n_pages) {
+        if constexpr (VA) nva = __ldg(desc.vaddrs + page + stride);
+        if constexpr (PA) npid = __ldg(desc.pids + page + stride);
       }
-    } else {
-      // this page's descriptor was fetched one page ago; fetch the next one
-      s[0] = static_cast<uint32_t>(nva);
-      s[1] = static_cast<uint32_t>(nva >> 32);
-      s[2] = npid;
-      if (page + stride < n_pages) desc_fetch(desc, page + stride, nva, npid);
-      if (!cached || s[1] != cached_hi || s[2] != cached_pid) {
-        c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
-        quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+    }
+    if (!cached || s[1] != cached_hi) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      cached_hi = s[1];
+      cached = true;
+    }
+    if constexpr (PA) {
+      if (!pid_cached || s[2] != cached_pid) {
         c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
         quarter_round<0>(c2a, c2b, c2c, c2d, rm);
-        cached_hi = s[1];
         cached_pid = s[2];
-        cached = true;
+        pid_cached = true;
       }
     }
     uint32_t x[16];

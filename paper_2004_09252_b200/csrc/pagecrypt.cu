@@ -172,7 +172,7 @@ unsigned pages_grid(size_t n_pages) {
     if constexpr (Variant == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
     else if constexpr (Variant == 2)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R, true>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R, 0>, 256, 0);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
     occ[dev] = o > 0 ? o : 1;
@@ -203,10 +203,14 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
       pc::PageDesc dd{d.vaddrs ? d.vaddrs + p0 : nullptr, d.pids ? d.pids + p0 : nullptr,
                       d.vaddr0 + 4096ull * p0, d.pid0};
       const unsigned grid = pages_grid<R, 2>(m);
-      if (!dd.vaddrs && !dd.pids)
-        pc::k_crypt_pages_async<R, true><<<grid, 256, 0, st>>>(key, dd, i4 + p0 * 256, o4 + p0 * 256, m);
-      else
-        pc::k_crypt_pages_async<R, false><<<grid, 256, 0, st>>>(key, dd, i4 + p0 * 256, o4 + p0 * 256, m);
+      const auto a = i4 + p0 * 256;
+      const auto b = o4 + p0 * 256;
+      switch ((dd.vaddrs ? 1 : 0) | (dd.pids ? 2 : 0)) {
+        case 0: pc::k_crypt_pages_async<R, 0><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
+        case 1: pc::k_crypt_pages_async<R, 1><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
+        case 2: pc::k_crypt_pages_async<R, 2><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
+        default: pc::k_crypt_pages_async<R, 3><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
+      }
       counted();
     }
   }
@@ -1309,8 +1313,10 @@ cudaError_t touch_rounds() {
   acc(touch(pc::k_crypt_pages<R>));
   acc(touch(pc::k_crypt_pages_coalesced<R>));
   acc(touch(pc::k_crypt_pages_tma<R, kTmaStages>));
-  acc(touch(pc::k_crypt_pages_async<R, true>));
-  acc(touch(pc::k_crypt_pages_async<R, false>));
+  acc(touch(pc::k_crypt_pages_async<R, 0>));
+  acc(touch(pc::k_crypt_pages_async<R, 1>));
+  acc(touch(pc::k_crypt_pages_async<R, 2>));
+  acc(touch(pc::k_crypt_pages_async<R, 3>));
   acc(touch(pc::k_keystream_seeds<R>));
   acc(touch(pc::k_service<R>));
   acc(touch(pc::k_slab_move<R, 0>));
