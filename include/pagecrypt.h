@@ -211,6 +211,11 @@ int pc_store_free_slots(pc_store *store, size_t *n);
  * before the refault frees its slots) run as get then put. */
 int pc_store_swap(pc_store *store, uint64_t client, uint32_t pid, const uint64_t *get_vaddrs, size_t n_get,
                   void *get_out, const uint64_t *put_vaddrs, size_t n_put, const void *put_in);
+/* fault: one orchestrator fault in one call -- vaddr is refaulted into out if
+ * stored (*refaulted = 1), else out is untouched (first touch, *refaulted =
+ * 0); evict_in (or NULL) is evicted to evict_vaddr; together one launch. */
+int pc_store_fault(pc_store *store, uint64_t client, uint32_t pid, uint64_t vaddr, void *out,
+                   uint64_t evict_vaddr, const void *evict_in, int *refaulted);
 
 /* ---- pinned host memory helpers ---------------------------------------
  * Note: freeing pinned memory (pc_host_free = cudaFreeHost) and

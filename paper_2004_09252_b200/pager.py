@@ -221,6 +221,9 @@ class WindowPager:
             raise ContractViolation(f"vaddr {v:#x} not page-aligned")
         if win.resident(v):
             raise ContractViolation(f"fault on resident page {v:#x}")
+        native = getattr(self.store, "fault", None)
+        if native is not None:
+            return self._fault_one_native(client, win, m, v, native)
         refault = self.store.contains(client, v)
         e = win.admit(v)
         try:
@@ -243,6 +246,32 @@ class WindowPager:
         except BaseException:
             win.undo_admits([v], [e])
             raise
+        m.faults += 1
+        if refault:
+            m.decrypt_ops += 1
+        else:
+            m.first_touch_faults += 1
+        if e is not None:
+            m.evictions += 1
+            m.encrypt_ops += 1
+        return out
+
+    def _fault_one_native(self, client, win, m, v, native) -> np.ndarray:
+        """The single fault as one store call (``DevicePageStore.fault``):
+        lookup, refault and the forced eviction in one native call and one
+        GPU round trip."""
+        e = win.admit(v)
+        out = np.zeros((1, PAGE_SIZE), dtype=np.uint8)  # stays zero on a first touch
+        try:
+            plain_ev = self._from_client(client, [e])[0] if e is not None else None
+            refault = native(client, v, out[0], e, plain_ev)
+            if plain_ev is not None:
+                plain_ev.fill(0)  # scratch_evict.wipe(), orchestrator.py:239
+        except BaseException:
+            win.undo_admits([v], [e])
+            raise
+        if refault or e is not None:
+            m.gpu_batches += 1
         m.faults += 1
         if refault:
             m.decrypt_ops += 1

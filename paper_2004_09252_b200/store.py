@@ -218,3 +218,26 @@ class DevicePageStore:
         self._call("pc_store_swap", self._h, _cid(client), client.pid, _p(gv), gv.size,
                    _p(out), _p(pv), pv.size, _p(arr))
         return out
+
+    def fault(self, client, vaddr: int, out: np.ndarray, evict_vaddr: int | None = None, evict_plain=None) -> bool:
+        """One orchestrator fault (``orchestrator.py:175-240``) in one call:
+        refault ``vaddr`` into ``out`` (uint8[4096]) if it is stored and return
+        True, else leave ``out`` untouched (a first touch) and return False;
+        evict ``evict_plain`` to ``evict_vaddr`` if given.  Refault and
+        eviction share one GPU round trip."""
+        self._need_key()
+        if vaddr % PAGE_SIZE or not 0 <= vaddr < 2**64:
+            raise ContractViolation(f"vaddr {vaddr:#x} not a page-aligned u64")
+        if out.nbytes != PAGE_SIZE or not out.flags.c_contiguous or not out.flags.writeable:
+            raise ContractViolation("out must be a writable C-contiguous 4096-byte array")
+        ev = None
+        if evict_plain is not None:
+            if evict_vaddr is None or evict_vaddr % PAGE_SIZE or not 0 <= evict_vaddr < 2**64:
+                raise ContractViolation("evict_vaddr must be a page-aligned u64")
+            ev = evict_plain if isinstance(evict_plain, np.ndarray) else np.frombuffer(evict_plain, np.uint8)
+            if ev.nbytes != PAGE_SIZE or not ev.flags.c_contiguous:
+                raise ContractViolation("evict_plain must be 4096 contiguous bytes")
+        flag = ctypes.c_int()
+        self._call("pc_store_fault", self._h, _cid(client), client.pid, vaddr, _addr(out),
+                   evict_vaddr or 0, None if ev is None else ev.ctypes.data, ctypes.byref(flag))
+        return bool(flag.value)

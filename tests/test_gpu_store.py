@@ -292,3 +292,22 @@ def test_stored_ciphertext_histogram(dkey):
     chi2 = float(((counts - expect) ** 2 / expect).sum())
     assert chi2 < 400  # 255 dof: mean 255, sd ~22.6
     s.close()
+
+
+def test_native_fault_entry(dkey):
+    """DevicePageStore.fault (pc_store_fault): one orchestrator fault --
+    lookup, refault and the forced eviction -- in one call."""
+    s = DevicePageStore(8, dkey)
+    out = np.full(4096, 7, np.uint8)
+    assert s.fault(C1, 0x1000, out) is False and (out == 7).all()  # first touch: untouched
+    assert s.fault(C1, 0x2000, out, 0x1000, np.frombuffer(page(1), np.uint8)) is False
+    assert s.lookup(C1, 0x1000) == pc.crypt_page(KEY, 0x1000, C1.pid, page(1))
+    # refault 0x1000 while evicting 0x2000: one launch
+    assert s.fault(C1, 0x1000, out, 0x2000, np.frombuffer(page(2), np.uint8)) is True
+    assert out.tobytes() == page(1)
+    assert not s.contains(C1, 0x1000) and s.refault(C1, 0x2000) == page(2)
+    assert s.free_slots == 8
+    with pytest.raises(ContractViolation):
+        s.fault(C1, 0x1001, out)
+    with pytest.raises(ContractViolation):
+        s.fault(C1, 0x1000, out, 0x3000, np.zeros(100, np.uint8))
