@@ -416,7 +416,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // per-page vaddr array, bit 1 = a per-page pid array, so no loop carries a
 // null-pointer test and a scalar pid keeps its column round hoisted.
 template <int ROUNDS, int DM>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, (DM == 0 || ROUNDS > 12) ? 4 : 3) // two descriptor sets need registers
 k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
                     uint32_t n_pages) {
   constexpr bool CONTIG = DM == 0;
@@ -469,6 +469,8 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
   if constexpr (PA) npid = __ldg(desc.pids + page);
   bool pid_cached = false;
   int st = 0;
+  // (unrolled over page pairs only where the loop stays small: R <= 12)
+  if constexpr (CONTIG || ROUNDS > 12) {
   for (;;) {
     issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
     uint32_t s[3];
@@ -524,6 +526,77 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     dst += step;
     va += va_step;
     st = st == 2 ? 0 : st + 1;
+  }
+  } else {
+    // Descriptor arrays: two register sets, each loaded two pages before its
+    // use and refilled right after it, the loop unrolled over the pair -- one
+    // loop-carried set had to be copied at the loop end and stalled there on
+    // its own load (ncu long_scoreboard).
+    uint64_t va_a = nva, va_b = 0;
+    uint32_t pid_a = npid, pid_b = desc.pid0;
+    if (page + stride < n_pages) {
+      if constexpr (VA) va_b = __ldg(desc.vaddrs + page + stride);
+      if constexpr (PA) pid_b = __ldg(desc.pids + page + stride);
+    }
+    auto one_page = [&](uint64_t &rv, uint32_t &rp) -> bool {
+      uint32_t s[3];
+      const uint64_t v = VA ? rv : va;
+      s[0] = static_cast<uint32_t>(v);
+      s[1] = static_cast<uint32_t>(v >> 32);
+      s[2] = PA ? rp : desc.pid0;
+      if (page + 2 * stride < n_pages) {
+        if constexpr (VA) rv = __ldg(desc.vaddrs + page + 2 * stride);
+        if constexpr (PA) rp = __ldg(desc.pids + page + 2 * stride);
+      }
+      issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
+    if (!cached || s[1] != cached_hi) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      cached_hi = s[1];
+      cached = true;
+    }
+    if constexpr (PA) {
+      if (!pid_cached || s[2] != cached_pid) {
+        c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+        quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+        cached_pid = s[2];
+        pid_cached = true;
+      }
+    }
+    uint32_t x[16];
+    x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
+    quarter_round<0>(x[0], x[4], x[8], x[12], rm);
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int r = 1; r < ROUNDS / 2; ++r) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    cp_async_wait<2>(); // this page's group has landed
+    const uint4 *mine = &ring[st][tid * 4];
+    const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]),
+                              d3.w ^ (x[15] + b)));
+      page += stride;
+      if (page >= n_pages) return false;
+      dst += step;
+      va += va_step;
+      st = st == 2 ? 0 : st + 1;
+      return true;
+    };
+    for (;;) {
+      if (!one_page(va_a, pid_a)) break;
+      if (!one_page(va_b, pid_b)) break;
+    }
   }
   cp_async_wait<0>();
 }
