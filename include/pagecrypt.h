@@ -200,6 +200,7 @@ int pc_store_get(pc_store *store, uint64_t client, uint32_t pid, const uint64_t 
 int pc_store_remove(pc_store *store, uint64_t client, const uint64_t *vaddrs, size_t n);
 int pc_store_drop_client(pc_store *store, uint64_t client);
 int pc_store_contains(pc_store *store, uint64_t client, uint64_t vaddr, int *found);
+int pc_store_contains_many(pc_store *store, uint64_t client, const uint64_t *vaddrs, size_t n, uint8_t *found);
 int pc_store_list(pc_store *store, uint64_t client, uint64_t *vaddrs, size_t cap, size_t *n);
 int pc_store_free_slots(pc_store *store, size_t *n);
 /* swap: one fault of the orchestrator (handle_fault + evict_page,

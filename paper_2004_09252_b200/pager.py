@@ -160,7 +160,11 @@ class WindowPager:
         out = np.zeros((k, PAGE_SIZE), dtype=np.uint8)  # first touch: zero pages
         if not k:
             return out
-        refault_idx = [i for i, v in enumerate(vlist) if self.store.contains(client, v)]
+        many = getattr(self.store, "contains_many", None)
+        if many is not None:  # one native lookup for the whole batch
+            refault_idx = np.flatnonzero(many(client, vlist)).tolist()
+        else:
+            refault_idx = [i for i, v in enumerate(vlist) if self.store.contains(client, v)]
         batch_pos = {v: i for i, v in enumerate(vlist)}
         # window admission in fault order (host state only); collect evictions
         # and keep an undo log (admission i evicted undo[i] or None)

@@ -135,6 +135,14 @@ class DevicePageStore:
         _native.call("pc_store_contains", self._h, _cid(client), int(vaddr) & (2**64 - 1), ctypes.byref(f))
         return bool(f.value)
 
+    def contains_many(self, client, vaddrs) -> np.ndarray:
+        """contains() for a batch, in one native call: bool[n]."""
+        va = self._vaddrs(vaddrs)
+        found = np.zeros(va.size, dtype=np.uint8)
+        if va.size:
+            _native.call("pc_store_contains_many", self._h, _cid(client), _p(va), va.size, _p(found))
+        return found.astype(bool)
+
     def drop_client(self, client) -> None:
         """Remove and wipe every entry of a client.  Unknown client: no-op."""
         _native.call("pc_store_drop_client", self._h, _cid(client))
