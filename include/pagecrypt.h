@@ -207,7 +207,7 @@ int pc_store_free_slots(pc_store *store, size_t *n);
  * pkg/src/pagecrypt/orchestrator.py:175-240) in one GPU round trip --
  * refault get_vaddrs into get_out (decrypt, remove, slots zeroed) and evict
  * put_in to put_vaddrs (encrypt, insert).  Same result as get(1, 1) then
- * put(1).  Up to 64 pages in total are one zero-copy launch and
+ * put(1).  Up to 128 pages in total are one zero-copy launch and
  * all-or-nothing; larger batches (or a slab too full to take the evictions
  * before the refault frees its slots) run as get then put. */
 int pc_store_swap(pc_store *store, uint64_t client, uint32_t pid, const uint64_t *get_vaddrs, size_t n_get,

@@ -34,7 +34,7 @@ from .errors import ContractViolation
 from .store import DevicePageStore
 
 PAGE_SIZE = 4096
-FUSED_MAX = 64  # pages per pc_store_swap launch (refaults + evictions)
+FUSED_MAX = 128  # pages per pc_store_swap launch (refaults + evictions)
 
 
 class SlidingWindow:

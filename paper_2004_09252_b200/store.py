@@ -210,7 +210,7 @@ class DevicePageStore:
         """Refault ``refault_vaddrs`` (decrypt out of HBM, remove) and evict
         ``evict_plains`` to ``evict_vaddrs`` (encrypt into HBM) -- one fault of
         the orchestrator (``orchestrator.py:175-240``) -- in one GPU round trip
-        for up to 64 pages in total.  Same result as ``refault_many`` then
+        for up to 128 pages in total.  Same result as ``refault_many`` then
         ``evict_many``.  Returns the refaulted plaintexts."""
         self._need_key()
         gv = self._vaddrs(refault_vaddrs)

@@ -189,12 +189,13 @@ def test_swap_matches_refault_then_evict(dkey, rounds):
     """swap == refault_many followed by evict_many: same plaintexts out, same
     ciphertext stored (the oracle's), same slot accounting."""
     rng = np.random.default_rng(rounds)
-    s = DevicePageStore(256, dkey, rounds=rounds)
+    s = DevicePageStore(512, dkey, rounds=rounds)
     c = ClientId(77, 3)
-    va = [0x1_0000_0000 + 4096 * i for i in range(40)]
-    plains = rng.integers(0, 256, size=(40, 4096), dtype=np.uint8)
+    va = [0x1_0000_0000 + 4096 * i for i in range(300)]
+    plains = rng.integers(0, 256, size=(300, 4096), dtype=np.uint8)
     s.evict_many(c, va[:20], plains[:20])
-    for n_get, n_put in ((1, 1), (0, 3), (5, 0), (7, 9), (20, 20)):
+    for n_get, n_put in ((1, 1), (0, 3), (5, 0), (7, 9), (20, 20), (20, 108), (64, 64), (100, 100)):
+        # fused up to 128 pages in total, refault-then-evict above
         get = [v for v in va if s.contains(c, v)][:n_get]
         put = [v for v in va if not s.contains(c, v)][:n_put]
         want_out = np.stack([plains[va.index(v)] for v in get]) if get else np.empty((0, 4096), np.uint8)
