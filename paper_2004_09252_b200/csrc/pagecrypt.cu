@@ -926,8 +926,13 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   {
     std::vector<size_t> sizes;
     size_t left = n;
-    const size_t ramp[3] = {C / 8, C / 4, C / 2};
-    const bool do_ramp = C >= 64 && n >= 4 * C;
+    // ramp: powers of two from 1024 pages (4 MiB) up to C/2, so the first
+    // transfer is small whatever the steady-state chunk is
+    std::vector<size_t> ramp;
+    for (size_t r = std::min<size_t>(1024, C / 8); r < C; r *= 2) ramp.push_back(r);
+    size_t ramp_sum = 0;
+    for (size_t r : ramp) ramp_sum += r;
+    const bool do_ramp = C >= 64 && n >= 2 * ramp_sum + 2 * C;
     std::vector<size_t> tail;
     if (do_ramp) {
       for (size_t r : ramp) { sizes.push_back(r); left -= r; }
