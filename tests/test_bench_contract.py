@@ -1,0 +1,45 @@
+"""The driver's bench contract, checked where it can be without a GPU: the
+reference arm (``bench.py --impl reference``) runs on host cores only and
+must print one JSON line with the agreed keys; under a multi-rank launch
+only rank 0 prints."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run_bench(*args, env=None):
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                          timeout=300, env=e, cwd=ROOT)
+
+
+def test_reference_arm_line():
+    r = run_bench("--impl", "reference", "--steps", "3", "--warmup", "3", "--ref-pages", "1024")
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["metric"].startswith("GB/s of pages") and d["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["config"]["rounds"] == 20 and d["config"]["pages_per_gpu"] == 262144
+
+
+def test_reference_arm_other_ranks_are_silent():
+    r = run_bench("--impl", "reference", "--steps", "3", "--warmup", "3", "--ref-pages", "64",
+                  env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 0, r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_warmup_below_three_is_refused():
+    r = run_bench("--impl", "reference", "--steps", "3", "--warmup", "2")
+    assert r.returncode != 0
