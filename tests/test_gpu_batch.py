@@ -438,3 +438,33 @@ class TestConcurrentCallers:
         assert not errors, errors
         assert store.free_slots == 4096
         store.close()
+
+
+class TestEdgeShapes:
+    def test_fewer_pages_than_engines(self, dkey, cuda):
+        """Engines whose range is empty do nothing; the rest still match."""
+        devs = [0, 0, 0, 0]
+        engines = [pc.Engine(d, n_streams=3, chunk_pages=64) for d in devs]
+        keys = [pc.DeviceKey.install(KEY, d) for d in devs]
+        try:
+            for n in (1, 2, 3):
+                pages = rand_pages(n, 40 + n)
+                got = partition.crypt_pages_multi(keys, engines, BASE, 2, pages)
+                assert np.array_equal(got, C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=2))
+        finally:
+            for k in keys:
+                k.destroy()
+            for e in engines:
+                e.destroy()
+
+    @pytest.mark.parametrize("n", [0, 1, 5])
+    def test_tiny_and_empty_device_batches_every_kernel(self, dkey, n, knob):
+        import torch
+
+        for kernel in (1, 2, 3, 4, 5):
+            knob("kernel", kernel)
+            pages = rand_pages(n, 50 + n) if n else np.empty((0, 4096), np.uint8)
+            got = pc.crypt_pages(dkey, BASE, 3, torch.from_numpy(pages).cuda())
+            torch.cuda.synchronize()
+            want = C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=3) if n else pages
+            assert np.array_equal(got.cpu().numpy(), want), kernel

@@ -135,6 +135,33 @@ class TestPool:
         assert pool.in_flight == 0
         pool.shutdown()
 
+    def test_single_slot_ring_many_producers(self, cuda):
+        """ring_capacity=1: every request waits for the previous one's slot;
+        four producer threads on one worker still all complete correctly."""
+        import threading
+
+        pool = make_pool(1, ring_capacity=1)
+        errors = []
+
+        def prod(t):
+            try:
+                for i in range(60):
+                    plain = bytes([t, i]) * (PAGE_SIZE // 2)
+                    p = Page(plain)
+                    pool.crypt(ClientId(70 + t, 0), 4096 * i, "encrypt", p)
+                    assert bytes(p.data) == O.crypt_page(KEY, 4096 * i, 70 + t, plain)
+            except BaseException as exc:
+                errors.append(repr(exc))
+
+        th = [threading.Thread(target=prod, args=(t,)) for t in range(4)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        assert not errors, errors
+        assert pool.in_flight == 0
+        pool.shutdown()
+
     def test_unwaited_requests_do_not_block_shutdown(self, cuda):
         pool = make_pool(2)
         pages = [Page() for _ in range(10)]
