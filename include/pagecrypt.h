@@ -128,7 +128,7 @@ int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, i
  * The paper's GPU design and the B200 replacement of the
  * reference's WorkerPool / WorkerRing / Completion
  * (pkg/src/pagecrypt/workers.py:28-254): one persistent kernel whose
- * n_workers 32-thread CTAs each serve a multiple-producer ring of ring_slots
+ * n_workers 64-thread CTAs each serve a multiple-producer ring of ring_slots
  * (power of two) requests in mapped pinned host memory.  The key is read
  * into the workers' registers once; after pc_service_start returns the
  * pc_key may be destroyed and the key then exists only in registers.

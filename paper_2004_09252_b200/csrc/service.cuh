@@ -9,7 +9,8 @@
 // (/root/reference/PAPER.md:615-632).  The reference emulates it with
 // WorkerPool / WorkerRing / Completion (pkg/src/pagecrypt/workers.py:28-254).
 //
-// Here: one 32-thread CTA per worker plus one dispatcher CTA.  Each worker
+// Here: one 64-thread CTA per worker (thread t makes block t of the page,
+// so a page is one pass) plus one dispatcher warp.  Each worker
 // owns a ring of C slots in mapped pinned host memory: a 64-byte header
 // (vaddr, pid, done_seq) and a 4 KiB page.  Request t of a worker lives in
 // slot t % C.  Producers publish tickets in order per worker by storing

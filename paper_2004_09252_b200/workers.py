@@ -5,7 +5,7 @@ The reference emulates MemShield's GPU service with Python threads
 MPSC ring (``WorkerRing``), a private 32-byte key slot, client-affine routing
 and a ``Completion`` per request.  This is the real thing on the B200
 (``include/pagecrypt.h`` section vii, ``csrc/service.cuh``): one persistent
-kernel whose 32-thread CTAs are the workers, rings in mapped pinned host
+kernel whose 64-thread CTAs are the workers, rings in mapped pinned host
 memory, and the key held only in the workers' registers -- the device copy
 used to start the kernel is destroyed as soon as every worker has loaded it
 (PAPER.md:592-594,624-637).
