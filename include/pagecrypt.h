@@ -95,6 +95,13 @@ int pc_key_device(const pc_key *key, int *device);
 int pc_crypt_pages_dev(const pc_key *key, const uint64_t *vaddrs, const uint32_t *pids,
                        uint64_t vaddr0, uint32_t pid0, const void *in, void *out,
                        size_t n, int rounds, void *stream);
+/* Device-side validation of descriptor arrays for (iv), stream-ordered and
+ * synchronous: *flags bit 0 = a vaddr is not page-aligned, bit 1 = a 64-bit
+ * pid (pids64, may be NULL) is outside u32; 64-bit pids are narrowed into
+ * pids32.  One library kernel -- never a foreign one, so it is safe beside
+ * the persistent worker service. */
+int pc_desc_check(const uint64_t *vaddrs, const int64_t *pids64, uint32_t *pids32, size_t n, void *stream,
+                  uint32_t *flags);
 
 /* ---- (v) host-resident batch -------------------------------------------
  * Same result over host buffers.  Pinned buffers (pc_host_alloc /

@@ -42,6 +42,7 @@ SIGNATURES = {
     "pc_key_device": (c_int, [c_void_p, P(c_int)]),
     "pc_crypt_pages_dev": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, c_u32, c_void_p, c_void_p,
                                    c_size_t, c_int, c_void_p]),
+    "pc_desc_check": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, P(c_u32)]),
     "pc_engine_create": (c_int, [c_int, c_int, c_size_t, P(c_void_p)]),
     "pc_engine_destroy": (c_int, [c_void_p]),
     "pc_crypt_pages_host": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_u64, c_u32,

@@ -673,6 +673,27 @@ k_slab_swap(const uint32_t *__restrict__ key, PageDesc desc, const uint32_t *__r
   st_v4(dst, d0); st_v4(dst + 1, d1); st_v4(dst + 2, d2); st_v4(dst + 3, d3);
 }
 
+// Descriptor validation on the device (crypt_pages' checks): flags bit 0 =
+// some vaddr is not page-aligned, bit 1 = some 64-bit pid is outside u32;
+// 64-bit pids are narrowed into pids32.  A library kernel (preloaded), so the
+// checks never launch a foreign kernel beside the persistent worker service.
+__global__ void __launch_bounds__(256)
+k_desc_check(const uint64_t *__restrict__ vaddrs, const int64_t *__restrict__ pids64, uint32_t *pids32, uint64_t n,
+             uint32_t *flags) {
+  uint32_t f = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (vaddrs && (__ldg(vaddrs + i) & 4095u)) f |= 1u;
+    if (pids64) {
+      const int64_t p = __ldg(pids64 + i);
+      if (p < 0 || p > 0xFFFFFFFFll) f |= 2u;
+      pids32[i] = static_cast<uint32_t>(p);
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
 // Zero the given slab slots (freed store entries are wiped, store.py:86-92).
 __global__ void __launch_bounds__(256)
 k_slab_wipe(const uint32_t *__restrict__ slots, uint4 *slab, uint64_t n_chunks) {

@@ -1255,6 +1255,37 @@ extern "C" int pc_slab_wipe(pc_engine *e, void *slab, size_t slab_pages, const u
 
 extern "C" {
 // ---- (vi) multi-device partition --------------------------------------------
+int pc_desc_check(const uint64_t *vaddrs, const int64_t *pids64, uint32_t *pids32, size_t n, void *stream,
+                  uint32_t *flags) {
+  if (!flags) return fail(PC_EINVAL, "flags is NULL");
+  *flags = 0;
+  if (n == 0 || (!vaddrs && !pids64)) return PC_OK;
+  if (pids64 && !pids32) return fail(PC_EINVAL, "pids32 is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  Scratch &sc = scratch(dev);
+  std::lock_guard<std::mutex> lk(sc.mu);
+  int rc = scratch_reserve(sc, 256);
+  if (rc != PC_OK) return rc;
+  uint32_t *d_flag = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void **>(&d_flag), 4, st)); // stream-ordered: safe beside the service
+  cudaError_t e = cudaMemsetAsync(d_flag, 0, 4, st);
+  if (e == cudaSuccess) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4096));
+    pc::k_desc_check<<<grid, 256, 0, st>>>(vaddrs, pids64, pids32, n, d_flag);
+    counted();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sc.h, d_flag, 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e2 = cudaFreeAsync(d_flag, st);
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
+  CU(e);
+  std::memcpy(flags, sc.h, 4);
+  return PC_OK;
+}
+
 int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, int n_dev,
                          const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0, uint32_t pid0,
                          const void *in, void *out, size_t n, int rounds) {
@@ -1339,6 +1370,7 @@ extern "C" int pc_preload(int device) {
   CU(touch_rounds<20>());
   CU(touch(pc::k_keygen));
   CU(touch(pc::k_slab_wipe));
+  CU(touch(pc::k_desc_check));
   CU(touch(pc::k_intpeak<0>));
   CU(touch(pc::k_intpeak<1>));
   CU(touch(pc::k_intpeak<2>));

@@ -364,6 +364,12 @@ def _crypt_pages_host(key, vaddrs, pids, pages, rounds, out, engine):
     return out
 
 
+def _desc_flags(vaddrs_ptr, pids64_ptr, pids32_ptr, n: int, stream_handle) -> int:
+    flags = ctypes.c_uint32()
+    _native.call("pc_desc_check", vaddrs_ptr, pids64_ptr, pids32_ptr, n, stream_handle, ctypes.byref(flags))
+    return flags.value
+
+
 def _crypt_pages_device(key, vaddrs, pids, pages, rounds, out, stream, check):
     import torch
 
@@ -398,7 +404,7 @@ def _crypt_pages_device(key, vaddrs, pids, pages, rounds, out, stream, check):
             raise ContractViolation("vaddrs must be n 64-bit integers")
         else:
             vaddrs = vaddrs.to(pages.device).contiguous()
-            if check and bool(((vaddrs.view(torch.int64) & (PAGE_SIZE - 1)) != 0).any()):
+            if check and _desc_flags(vaddrs.data_ptr(), None, None, n, sh) & 1:
                 raise ContractViolation("vaddr not page-aligned")
         keep.append(vaddrs)
         v_ptr = vaddrs.data_ptr()
@@ -412,11 +418,16 @@ def _crypt_pages_device(key, vaddrs, pids, pages, rounds, out, stream, check):
         elif pids.numel() != n:
             raise ContractViolation("need n pids")
         else:
-            if pids.element_size() != 4:
-                if check and bool(((pids < 0) | (pids >= 2**32)).any()):
-                    raise ContractViolation("pid not a u32")
-                pids = pids.to(torch.int64).to(torch.int32)  # wraps to u32 bits
             pids = pids.to(pages.device).contiguous()
+            if pids.element_size() != 4:
+                if pids.element_size() != 8 or pids.dtype.is_floating_point:
+                    raise ContractViolation("pids must be 32- or 64-bit integers")
+                # narrowed (and range-checked) by a library kernel: no torch
+                # kernel launches here, so this is safe beside the worker service
+                p32 = torch.empty(n, dtype=torch.int32, device=pages.device)
+                if _desc_flags(None, pids.data_ptr(), p32.data_ptr(), n, sh) & 2 and check:
+                    raise ContractViolation("pid not a u32")
+                pids = p32
         keep.append(pids)
         p_ptr = pids.data_ptr()
 

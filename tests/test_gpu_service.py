@@ -428,3 +428,44 @@ def test_completion_signal_after_gpu_release(cuda):
         ok.wait()
     finally:
         pool.shutdown()
+
+
+def test_device_checks_never_launch_foreign_kernels_beside_the_service(cuda, tmp_path):
+    """With the persistent service up, crypt_pages on device descriptor
+    arrays (incl. 64-bit pids to narrow and check) must not launch a kernel
+    the library did not preload: a fresh process (nothing of torch loaded)
+    would otherwise hang forever on its first torch kernel."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "beside_service.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_2004_09252_b200 as pc\n"
+        "from paper_2004_09252_b200.workers import WorkerPool, ClientId\n"
+        "from oracle import coracle as C\n"
+        "KEY = bytes(range(32))\n"
+        "pool = WorkerPool(n_workers=4, keysource=lambda n: KEY)\n"
+        "k = pc.DeviceKey.install(KEY, 0)\n"
+        "n = 300\n"
+        "pages = np.random.default_rng(1).integers(0, 256, size=(n, 4096), dtype=np.uint8)\n"
+        "va = (0x100000000 + 4096 * np.arange(n)).astype(np.uint64)\n"
+        "pid = (7 + np.arange(n) % 5).astype(np.int64)\n"
+        "got = pc.crypt_pages(k, torch.from_numpy(va.view(np.int64)).cuda(), torch.from_numpy(pid).cuda(),\n"
+        "                     torch.from_numpy(pages).cuda())\n"
+        "torch.cuda.current_stream().synchronize()\n"
+        "assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, va, pid.astype(np.uint32), pages))\n"
+        "try:\n"
+        "    pc.crypt_pages(k, torch.from_numpy((va + 1).view(np.int64)).cuda(), 1, torch.from_numpy(pages).cuda())\n"
+        "    raise SystemExit('unaligned vaddr accepted')\n"
+        "except pc.ContractViolation:\n"
+        "    pass\n"
+        "k.destroy(); pool.shutdown(); print('ok')\n")
+    env = dict(os.environ)
+    env.pop("CUDA_MODULE_LOADING", None)  # the default lazy loading, where the hazard lives
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=180, env=env,
+                       cwd=root)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.returncode, r.stdout[-500:], r.stderr[-1500:])
