@@ -24,6 +24,8 @@ import torch  # noqa: E402
 
 import paper_2004_09252_b200 as pc  # noqa: E402
 from paper_2004_09252_b200 import _chacha_cuda  # noqa: E402
+from paper_2004_09252_b200 import partition  # noqa: E402
+from paper_2004_09252_b200.pager import WindowPager  # noqa: E402
 from paper_2004_09252_b200.store import DevicePageStore  # noqa: E402
 from paper_2004_09252_b200.workers import ClientId, WorkerPool  # noqa: E402
 from oracle import coracle as C  # noqa: E402
@@ -54,6 +56,7 @@ def main():
         bool(((wv & 4095) != 0).any())
     torch.cuda.synchronize()
     dkey = pc.DeviceKey.install(KEY, 0)
+    engines = [pc.Engine(0, n_streams=3, chunk_pages=512) for _ in range(2)]
     pool = None if a.no_service else WorkerPool(n_workers=8, keysource=lambda n: KEY)
     store = DevicePageStore(1 << 15, dkey)
     counts = {}
@@ -73,9 +76,13 @@ def main():
         client = ClientId(1000 + t, 0)
         stored = {}
         spare = [0]
+        pclient = ClientId(5000 + t, 0)
+        pmem, pseen = {}, {}
+        pager = WindowPager(store, lambda c, vs: np.stack([np.frombuffer(pmem.pop(v), np.uint8) for v in vs]), 4)
+        pager.register(pclient)
         try:
             while time.time() < deadline and not errors:
-                op = rng.randrange(6)
+                op = rng.randrange(9)
                 if op == 3 and pool is None:
                     continue
                 with lock:
@@ -134,6 +141,37 @@ def main():
                         c.wait()
                     assert bytes(buf) == want.tobytes(), "service"
                     bump("service")
+                elif op == 6:  # key lifecycle: a fresh key, a batch with it, destroyed
+                    kb = bytes(nrng.integers(0, 256, 32, dtype=np.uint8))
+                    pages = nrng.integers(0, 256, size=(rng.choice([1, 70, 600]), 4096), dtype=np.uint8)
+                    with pc.DeviceKey.install(kb, 0) as k2:
+                        with torch.cuda.stream(stream):
+                            got = pc.crypt_pages(k2, 0x5000, t, torch.from_numpy(pages).cuda(), stream=stream)
+                        stream.synchronize()
+                        assert np.array_equal(got.cpu().numpy(), C.crypt_pages(kb, None, None, pages, vaddr0=0x5000,
+                                                                              pid0=t, nthreads=2)), "fresh key"
+                    bump("key_lifecycle")
+                elif op == 7:  # pager faults on this thread's client (window 4), client memory as the model
+                    v = 0x3_0000_0000 + 4096 * rng.randrange(12)
+                    if v in pmem:
+                        continue
+                    got = pager.fault(pclient, v)
+                    want = pseen.get(v, bytes(4096))
+                    assert got == want, "pager fault"
+                    data = bytearray(got)
+                    data[rng.randrange(4096)] ^= 0x5A
+                    pmem[v] = bytes(data)
+                    pseen[v] = bytes(data)
+                    bump("pager_fault")
+                elif op == 8:  # device-resident partition over two engines
+                    n = rng.choice([5, 300, 3000])
+                    pages = nrng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
+                    with torch.cuda.stream(stream):
+                        dpages = torch.from_numpy(pages).cuda()
+                    got = partition.crypt_pages_multi([dkey, dkey], engines, 0x9000, t, dpages)
+                    assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=0x9000,
+                                                                          pid0=t, nthreads=2)), "multi"
+                    bump("partition")
                 else:  # store
                     v = 0x1_0000_0000 + 4096 * rng.randrange(256)
                     page = nrng.integers(0, 256, 4096, dtype=np.uint8)
