@@ -180,8 +180,12 @@ def main():
                             assert np.array_equal(np.frombuffer(store.refault(client, v), np.uint8), stored.pop(v)), "refault"
                         else:
                             out = np.empty(4096, np.uint8)
-                            spare[0] += 1
-                            e = 0x2_0000_0000 + 4096 * spare[0]  # a page never stored before
+                            # evict a page of the same 256-page range that is not stored
+                            free = [x for x in (0x1_0000_0000 + 4096 * rng.randrange(256) for _ in range(8))
+                                    if x not in stored and x != v]
+                            if not free:
+                                continue
+                            e = free[0]
                             assert store.fault(client, v, out, e, page) is True, "fault: not refaulted"
                             assert np.array_equal(out, stored.pop(v)), "fault"
                             stored[e] = page
