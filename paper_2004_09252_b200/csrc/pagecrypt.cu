@@ -162,12 +162,18 @@ void launch_crypt_r(uint32_t mask, const uint32_t *key, const pc::PageDesc &d, c
 // by the number of 4-page slots.
 template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async
 unsigned pages_grid(size_t n_pages) {
+  // per-device launch geometry, computed once; the mutex makes the first
+  // use from several host threads safe (a racing reader saw sms set and occ
+  // still 0 -> grid 0 -> "invalid configuration", found by tools/soak.py)
   static int sms[64] = {0}, occ[64] = {0};
+  static std::mutex init_mu;
   int dev = 0;
   cudaGetDevice(&dev);
   dev &= 63;
+  std::lock_guard<std::mutex> init_lk(init_mu);
   if (!sms[dev]) {
-    cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    int n_sm = 0;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     int o = 0;
     if constexpr (Variant == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
@@ -176,6 +182,7 @@ unsigned pages_grid(size_t n_pages) {
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
     occ[dev] = o > 0 ? o : 1;
+    sms[dev] = n_sm;
   }
   // v5 at ChaCha12 runs best at 2 of its 4 resident CTAs per SM: 2835 vs
   // 2774 GB/s through bench.py (profiles/r01_ctas_ab.txt) -- fewer
@@ -255,16 +262,21 @@ template <int R>
 int launch_tma_r(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out, size_t n_pages,
                  cudaStream_t st) {
   static int sms[64] = {0}, occ[64] = {0};
+  static std::mutex init_mu; // first use from several threads (see pages_grid)
   int dev = 0;
   CU(cudaGetDevice(&dev));
   dev &= 63;
   auto kfn = pc::k_crypt_pages_tma<R, kTmaStages>;
-  if (!sms[dev]) {
-    CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem)));
-    CU(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-    int o = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, 256, kTmaSmem));
-    occ[dev] = o > 0 ? o : 1;
+  {
+    std::lock_guard<std::mutex> init_lk(init_mu);
+    if (!sms[dev]) {
+      CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem)));
+      int n_sm = 0, o = 0;
+      CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, 256, kTmaSmem));
+      occ[dev] = o > 0 ? o : 1;
+      sms[dev] = n_sm;
+    }
   }
   // TMA row coordinates are int32: split batches above 2^25 pages
   constexpr size_t kMaxPages = size_t(1) << 25;

@@ -468,3 +468,60 @@ class TestEdgeShapes:
             torch.cuda.synchronize()
             want = C.crypt_pages(KEY, None, None, pages, vaddr0=BASE, pid0=3) if n else pages
             assert np.array_equal(got.cpu().numpy(), want), kernel
+
+
+_FIRST_USE_CHILD = r"""
+import sys, threading
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import paper_2004_09252_b200 as pc
+from oracle import coracle as C
+KEY = bytes(range(32))
+torch.zeros(1, device="cuda"); torch.cuda.synchronize()
+dkey = pc.DeviceKey.install(KEY, 0)
+n_threads = 24
+bar = threading.Barrier(n_threads)
+bad = []
+def run(t):
+    rng = np.random.default_rng(t)
+    r = (8, 12, 20)[t % 3]
+    n = (1, 64, 700)[(t // 3) % 3]
+    pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
+    s = torch.cuda.Stream()
+    d = torch.from_numpy(pages).cuda()
+    torch.cuda.synchronize()
+    try:
+        bar.wait()
+        if t % 2:
+            with torch.cuda.stream(s):
+                got = pc.crypt_pages(dkey, 0x10000, t, d, rounds=r, stream=s)
+            s.synchronize()
+            got = got.cpu().numpy()
+        else:
+            got = np.asarray(pc.crypt_pages(dkey, 0x10000, t, pages, rounds=r))
+        if not np.array_equal(got, C.crypt_pages(KEY, None, None, pages, rounds=r, vaddr0=0x10000, pid0=t)):
+            bad.append((t, "mismatch"))
+    except Exception as e:
+        bad.append((t, repr(e)))
+th = [threading.Thread(target=run, args=(t,)) for t in range(n_threads)]
+[x.start() for x in th]; [x.join() for x in th]
+print("BAD", bad)
+"""
+
+
+@pytest.mark.parametrize("attempt", range(3))
+def test_concurrent_first_use_in_fresh_process(cuda, attempt):
+    """24 threads make their FIRST library call at the same instant (a
+    barrier), across round counts and host/device buffers, in a fresh
+    interpreter.  Regression for the lazily cached launch geometry
+    (pagecrypt.cu pages_grid): a racing thread once read the SM count set
+    but the occupancy still 0 and launched a grid of 0 CTAs."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _FIRST_USE_CHILD.format(root=root)], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "BAD []", out.stdout[-2000:]

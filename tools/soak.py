@@ -82,7 +82,7 @@ def main():
         pager.register(pclient)
         try:
             while time.time() < deadline and not errors:
-                op = rng.randrange(9)
+                op = rng.randrange(9) if rng.random() > 0.01 else 9
                 if op == 3 and pool is None:
                     continue
                 with lock:
@@ -172,6 +172,19 @@ def main():
                     assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, None, None, pages, vaddr0=0x9000,
                                                                           pid0=t, nthreads=2)), "multi"
                     bump("partition")
+                elif op == 9:  # a second, short-lived worker service beside the first
+                    kb = bytes(nrng.integers(0, 256, 32, dtype=np.uint8))
+                    p2 = WorkerPool(n_workers=2, keysource=lambda n: kb)
+                    try:
+                        for i in range(8):
+                            plain = nrng.integers(0, 256, 4096, dtype=np.uint8).tobytes()
+                            buf = bytearray(plain)
+                            p2.crypt(ClientId(9000 + t, 0), 4096 * i, "encrypt", buf)
+                            want = C.crypt_pages(kb, [4096 * i], 9000 + t, np.frombuffer(plain, np.uint8).reshape(1, 4096))[0]
+                            assert bytes(buf) == want.tobytes(), "second service"
+                    finally:
+                        p2.shutdown()
+                    bump("service_lifecycle")
                 else:  # store
                     v = 0x1_0000_0000 + 4096 * rng.randrange(256)
                     page = nrng.integers(0, 256, 4096, dtype=np.uint8)
