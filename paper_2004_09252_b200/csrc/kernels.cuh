@@ -490,7 +490,7 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
       cached_hi = s[1];
       cached = true;
     }
-    if constexpr (PA) {
+    if constexpr (PA) { // R=20 keeps the cached round (the unconditional one: 1678 vs 1735 GB/s)
       if (!pid_cached || s[2] != cached_pid) {
         c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
         quarter_round<0>(c2a, c2b, c2c, c2d, rm);
@@ -555,13 +555,9 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
       cached_hi = s[1];
       cached = true;
     }
-    if constexpr (PA) {
-      if (!pid_cached || s[2] != cached_pid) {
-        c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
-        quarter_round<0>(c2a, c2b, c2c, c2d, rm);
-        cached_pid = s[2];
-        pid_cached = true;
-      }
+    if constexpr (PA) { // every page, no branch: R=12 2537-2627 vs 2432-2558 GB/s (profiles/r01_desc_probe.txt)
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
     }
     uint32_t x[16];
     x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];

@@ -17,10 +17,13 @@ key = pc.DeviceKey.generate(0)
 va_seq = torch.from_numpy((0x100000000 + 4096 * np.arange(n, dtype=np.uint64)).view(np.int64)).cuda()
 va_perm = torch.from_numpy((0x100000000 + 4096 * np.random.default_rng(0).permutation(n).astype(np.uint64)).view(np.int64)).cuda()
 pids = torch.from_numpy((1 + np.arange(n) % 64).astype(np.int32)).cuda()
+pids1 = torch.ones(n, dtype=torch.int32, device="cuda")
 cases = {"contiguous, pid 1": (0x100000000, 1), "vaddr array (sequential), pid 1": (va_seq, 1),
+         "vaddr array (sequential), pid array of 1s": (va_seq, pids1),
          "vaddr array (sequential), pid = 1 + i % 64": (va_seq, pids),
          "vaddr array (permuted), pid = 1 + i % 64": (va_perm, pids)}
-for r in (20, 12, 8):
+rounds = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else (20, 12, 8)
+for r in rounds:
     for name, (v, p) in cases.items():
         for _ in range(3):
             pc.crypt_pages(key, v, p, pages, out=out, rounds=r, check=False)
