@@ -400,7 +400,7 @@ def _crypt_pages_device(key, vaddrs, pids, pages, rounds, out, stream, check):
         if not _is_torch(vaddrs):
             host, _ = _host_vaddrs(vaddrs, n)
             vaddrs = torch.from_numpy(host.view(np.int64)).to(pages.device, non_blocking=False)
-        elif vaddrs.numel() != n or vaddrs.element_size() != 8:
+        elif vaddrs.numel() != n or vaddrs.element_size() != 8 or vaddrs.dtype.is_floating_point:
             raise ContractViolation("vaddrs must be n 64-bit integers")
         else:
             vaddrs = vaddrs.to(pages.device).contiguous()
@@ -419,8 +419,10 @@ def _crypt_pages_device(key, vaddrs, pids, pages, rounds, out, stream, check):
             raise ContractViolation("need n pids")
         else:
             pids = pids.to(pages.device).contiguous()
+            if pids.dtype.is_floating_point or pids.dtype.is_complex or pids.dtype == torch.bool:
+                raise ContractViolation("pids must be 32- or 64-bit integers")
             if pids.element_size() != 4:
-                if pids.element_size() != 8 or pids.dtype.is_floating_point:
+                if pids.element_size() != 8:
                     raise ContractViolation("pids must be 32- or 64-bit integers")
                 # narrowed (and range-checked) by a library kernel: no torch
                 # kernel launches here, so this is safe beside the worker service
@@ -444,7 +446,7 @@ def _crypt_pages_device(key, vaddrs, pids, pages, rounds, out, stream, check):
             _native.call("pc_crypt_pages_dev", tmp.handle, v_ptr, p_ptr, vaddr0, pid0,
                          pages.data_ptr(), out.data_ptr(), n, rounds, sh)
         finally:
-            tmp.destroy()  # device-synchronises before zeroing
+            tmp.destroy()  # zeroed on the key's stream after the batch's use of it
     if keep:
         # keep descriptor tensors alive until the stream has used them
         for t in keep:

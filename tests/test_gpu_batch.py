@@ -141,6 +141,19 @@ class TestDevicePath:
         with pytest.raises(ContractViolation):
             pc.crypt_pages(dkey, v, 1, t(rand_pages(2)))
 
+    def test_float_device_descriptors_rejected(self, dkey):
+        """Descriptor tensors must hold integers: a float64 vaddr tensor has
+        the right element size but not the meaning."""
+        import torch
+
+        pages = t(rand_pages(2))
+        with pytest.raises(ContractViolation):
+            pc.crypt_pages(dkey, torch.tensor([4096.0, 8192.0], dtype=torch.float64, device="cuda"), 1, pages)
+        with pytest.raises(ContractViolation):
+            pc.crypt_pages(dkey, BASE, torch.tensor([1.0, 2.0], dtype=torch.float32, device="cuda"), pages)
+        with pytest.raises(ContractViolation):
+            pc.crypt_pages(dkey, BASE, torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda"), pages)
+
     def test_max_vaddr_and_pid(self, dkey):
         import torch
 
