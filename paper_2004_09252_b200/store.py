@@ -110,10 +110,8 @@ class DevicePageStore:
 
     def insert(self, client, vaddr: int, cipher) -> None:
         """Store a private copy of a ciphertext page.  Double insert is a bug."""
-        if vaddr % PAGE_SIZE:
-            raise ContractViolation(f"vaddr {vaddr:#x} not page-aligned")
+        va = self._vaddrs([vaddr])
         arr = self._page(cipher)
-        va = np.array([vaddr], dtype=np.uint64)
         self._call("pc_store_put", self._h, _cid(client), client.pid, _p(va), 1, _p(arr), 0)
 
     def lookup(self, client, vaddr: int):
@@ -121,18 +119,21 @@ class DevicePageStore:
         if not self.contains(client, vaddr):
             return None
         out = np.empty(PAGE_SIZE, dtype=np.uint8)
-        va = np.array([vaddr], dtype=np.uint64)
+        va = self._vaddrs([vaddr])
         self._call("pc_store_get", self._h, _cid(client), client.pid, _p(va), 1, _p(out), 0, 0)
         return out.tobytes()
 
     def remove(self, client, vaddr: int) -> None:
         """Delete an entry; the released slot is wiped before reuse."""
-        va = np.array([vaddr], dtype=np.uint64)
+        va = self._vaddrs([vaddr])
         self._call("pc_store_remove", self._h, _cid(client), _p(va), 1)
 
     def contains(self, client, vaddr: int) -> bool:
+        v = int(vaddr)
+        if not 0 <= v < 2**64 or v % PAGE_SIZE:
+            return False  # never stored (insert rejects it); a negative vaddr must not wrap onto a stored one
         f = ctypes.c_int()
-        _native.call("pc_store_contains", self._h, _cid(client), int(vaddr) & (2**64 - 1), ctypes.byref(f))
+        _native.call("pc_store_contains", self._h, _cid(client), v, ctypes.byref(f))
         return bool(f.value)
 
     def contains_many(self, client, vaddrs) -> np.ndarray:
@@ -200,8 +201,8 @@ class DevicePageStore:
         va = self._vaddrs(vaddrs)
         if out is None:
             out = np.empty((va.size, PAGE_SIZE), dtype=np.uint8)
-        elif out.nbytes != va.size * PAGE_SIZE or not out.flags.c_contiguous:
-            raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
+        elif out.nbytes != va.size * PAGE_SIZE or not out.flags.c_contiguous or not out.flags.writeable:
+            raise ContractViolation("out must be a writable C-contiguous uint8[n, 4096] buffer")
         self._call("pc_store_get", self._h, _cid(client), client.pid, _p(va), va.size,
                    _p(out), 1, 1)
         return out
@@ -221,8 +222,8 @@ class DevicePageStore:
             raise ContractViolation(f"{pv.size} vaddrs for {arr.shape[0]} pages")
         if out is None:
             out = np.empty((gv.size, PAGE_SIZE), dtype=np.uint8)
-        elif out.nbytes != gv.size * PAGE_SIZE or not out.flags.c_contiguous:
-            raise ContractViolation("out must be a C-contiguous uint8[n, 4096] buffer")
+        elif out.nbytes != gv.size * PAGE_SIZE or not out.flags.c_contiguous or not out.flags.writeable:
+            raise ContractViolation("out must be a writable C-contiguous uint8[n, 4096] buffer")
         self._call("pc_store_swap", self._h, _cid(client), client.pid, _p(gv), gv.size,
                    _p(out), _p(pv), pv.size, _p(arr))
         return out

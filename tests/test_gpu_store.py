@@ -312,3 +312,23 @@ def test_native_fault_entry(dkey):
         s.fault(C1, 0x1001, out)
     with pytest.raises(ContractViolation):
         s.fault(C1, 0x1000, out, 0x3000, np.zeros(100, np.uint8))
+
+
+def test_out_of_range_vaddrs_never_alias_stored_pages(dkey):
+    """contains/lookup of a vaddr the store can never hold (negative,
+    >= 2**64, unaligned) answer False/None like the reference's dict lookups
+    (store.py:67-86) -- in particular -4096 must not wrap onto
+    0xffff_ffff_ffff_f000 -- and insert/remove of one raise."""
+    s = DevicePageStore(8, dkey)
+    top = 2**64 - 4096
+    s.evict(C1, top, bytes(4096))
+    assert s.contains(C1, top)
+    for bad in (-4096, 2**64 + top, top + 1):
+        assert not s.contains(C1, bad)
+        assert s.lookup(C1, bad) is None
+        with pytest.raises(ContractViolation):
+            s.remove(C1, bad)
+        with pytest.raises(ContractViolation):
+            s.insert(C1, bad, bytes(4096))
+    assert s.refault(C1, top) == bytes(4096)
+    s.close()

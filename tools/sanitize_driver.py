@@ -31,14 +31,18 @@ def main():
     with pc.DeviceKey.install(KEY, 0) as k:
         for kern in (1, 2, 3, 4, 5):
             _native.tune("kernel", kern)
-            for r in (8, 20):
+            for r in (8, 12, 20):
                 d = torch.from_numpy(pages).cuda()
                 pc.crypt_pages(k, 0x1_0000_0000, 3, d, out=d, rounds=r)
                 want = C.crypt_pages(KEY, None, None, pages, rounds=r, vaddr0=0x1_0000_0000, pid0=3)
                 assert np.array_equal(d.cpu().numpy(), want), (kern, r)
-                got = pc.crypt_pages(k, torch.from_numpy(va.view(np.int64)).cuda(),
-                                     torch.from_numpy(pi.view(np.int32)).cuda(), torch.from_numpy(pages).cuda(), rounds=r)
-                assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, va, pi, pages, rounds=r)), (kern, r)
+                # every descriptor shape (vaddr array and/or pid array)
+                dva = torch.from_numpy(va.view(np.int64)).cuda()
+                dpi = torch.from_numpy(pi.view(np.int32)).cuda()
+                for v_arg, p_arg, v_ref, p_ref in ((dva, dpi, va, pi), (dva, 7, va, np.full(n, 7, np.uint32)),
+                                                   (0x5000, dpi, 0x5000 + 4096 * np.arange(n, dtype=np.uint64), pi)):
+                    got = pc.crypt_pages(k, v_arg, p_arg, torch.from_numpy(pages).cuda(), rounds=r)
+                    assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=r)), (kern, r)
         _native.tune("kernel", 0)
         for hm in (0, 1, 2, 3):
             _native.tune("host_mode", hm)
