@@ -469,8 +469,10 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
   if constexpr (PA) npid = __ldg(desc.pids + page);
   bool pid_cached = false;
   int st = 0;
-  // (unrolled over page pairs only where the loop stays small: R <= 12)
-  if constexpr (CONTIG || ROUNDS > 12) {
+  // (unrolled over page pairs where that pays: R <= 12, and R = 20 with a
+  // vaddr array only -- 1723 vs 1699 GB/s; with a pid array the R = 20 pair
+  // loop is slower, 1675 vs 1739, profiles/r01_desc_probe.txt)
+  if constexpr (CONTIG || (ROUNDS > 12 && DM != 1)) {
   for (;;) {
     issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
     uint32_t s[3];
