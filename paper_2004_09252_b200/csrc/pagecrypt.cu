@@ -158,38 +158,50 @@ void launch_crypt_r(uint32_t mask, const uint32_t *key, const pc::PageDesc &d, c
   }
 }
 
+// Per-device launch geometry, computed once and published as ONE atomic word
+// (SM count << 16 | resident CTAs per SM): a concurrent first caller once read
+// the SM count set and the occupancy still 0 -> grid 0 -> "invalid
+// configuration argument" (found by tools/soak.py).  Racing first callers
+// compute the same value; the hot path is one acquire load.
+template <typename Init> // Init(int &n_sm, int &occ) -> cudaError_t
+cudaError_t cached_geometry(std::atomic<uint32_t> (&cache)[64], int dev, int &n_sm, int &occ, Init init) {
+  uint32_t g = cache[dev & 63].load(std::memory_order_acquire);
+  if (!g) {
+    int s = 0, o = 0;
+    const cudaError_t e = init(s, o);
+    if (e != cudaSuccess) return e;
+    g = (static_cast<uint32_t>(s) << 16) | static_cast<uint32_t>(o > 0 ? o : 1);
+    cache[dev & 63].store(g, std::memory_order_release);
+  }
+  n_sm = static_cast<int>(g >> 16);
+  occ = static_cast<int>(g & 0xFFFF);
+  return cudaSuccess;
+}
+
 // Persistent grid for k_crypt_pages: SMs x resident CTAs (occupancy), capped
 // by the number of 4-page slots.
 template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async
 unsigned pages_grid(size_t n_pages) {
-  // per-device launch geometry, computed once; the mutex makes the first
-  // use from several host threads safe (a racing reader saw sms set and occ
-  // still 0 -> grid 0 -> "invalid configuration", found by tools/soak.py)
-  static int sms[64] = {0}, occ[64] = {0};
-  static std::mutex init_mu;
-  int dev = 0;
+  static std::atomic<uint32_t> geo[64] = {};
+  int dev = 0, n_sm = 0, occ = 0;
   cudaGetDevice(&dev);
-  dev &= 63;
-  std::lock_guard<std::mutex> init_lk(init_mu);
-  if (!sms[dev]) {
-    int n_sm = 0;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    int o = 0;
-    if constexpr (Variant == 1)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
-    else if constexpr (Variant == 2)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R, 0>, 256, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
-    occ[dev] = o > 0 ? o : 1;
-    sms[dev] = n_sm;
-  }
+  if (cached_geometry(geo, dev, n_sm, occ, [dev](int &s, int &o) {
+        cudaError_t e = cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        if constexpr (Variant == 1)
+          return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
+        else if constexpr (Variant == 2)
+          return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R, 0>, 256, 0);
+        else
+          return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
+      }) != cudaSuccess)
+    return 0; // the launch then fails loudly ("invalid configuration")
   // v5 at ChaCha12 runs best at 2 of its 4 resident CTAs per SM: 2835 vs
   // 2774 GB/s through bench.py (profiles/r01_ctas_ab.txt) -- fewer
   // concurrent page streams, same ALU feed (ILP 4 per thread)
-  const int dflt = (Variant == 2 && R == 12) ? std::min(occ[dev], 2) : occ[dev];
+  const int dflt = (Variant == 2 && R == 12) ? std::min(occ, 2) : occ;
   const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : dflt;
-  const uint64_t want = static_cast<uint64_t>(sms[dev]) * per_sm;
+  const uint64_t want = static_cast<uint64_t>(n_sm) * per_sm;
   const uint64_t slots = (n_pages + 3) / 4;
   return static_cast<unsigned>(std::min<uint64_t>(want, slots));
 }
@@ -261,23 +273,16 @@ int page_tensor_map(CUtensorMap *m, const void *base, uint64_t n_pages) {
 template <int R>
 int launch_tma_r(const uint32_t *key, const pc::PageDesc &d, const void *in, void *out, size_t n_pages,
                  cudaStream_t st) {
-  static int sms[64] = {0}, occ[64] = {0};
-  static std::mutex init_mu; // first use from several threads (see pages_grid)
-  int dev = 0;
+  static std::atomic<uint32_t> geo[64] = {};
+  int dev = 0, n_sm = 0, occ = 0;
   CU(cudaGetDevice(&dev));
-  dev &= 63;
   auto kfn = pc::k_crypt_pages_tma<R, kTmaStages>;
-  {
-    std::lock_guard<std::mutex> init_lk(init_mu);
-    if (!sms[dev]) {
-      CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem)));
-      int n_sm = 0, o = 0;
-      CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, 256, kTmaSmem));
-      occ[dev] = o > 0 ? o : 1;
-      sms[dev] = n_sm;
-    }
-  }
+  CU(cached_geometry(geo, dev, n_sm, occ, [dev, kfn](int &s, int &o) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, 256, kTmaSmem);
+    return e;
+  }));
   // TMA row coordinates are int32: split batches above 2^25 pages
   constexpr size_t kMaxPages = size_t(1) << 25;
   for (size_t p0 = 0; p0 < n_pages; p0 += kMaxPages) {
@@ -288,9 +293,9 @@ int launch_tma_r(const uint32_t *key, const pc::PageDesc &d, const void *in, voi
     if (rc != PC_OK) return rc;
     pc::PageDesc dd{d.vaddrs ? d.vaddrs + p0 : nullptr, d.pids ? d.pids + p0 : nullptr,
                     d.vaddr0 + 4096ull * p0, d.pid0};
-    const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : occ[dev];
+    const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : occ;
     const uint64_t slots = (m + 3) / 4;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(static_cast<uint64_t>(sms[dev]) * per_sm, slots));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(static_cast<uint64_t>(n_sm) * per_sm, slots));
     kfn<<<grid, 256, kTmaSmem, st>>>(tin, tout, key, dd, m);
     counted();
     CU(cudaGetLastError());
