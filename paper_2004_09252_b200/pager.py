@@ -112,6 +112,7 @@ class WindowPager:
             raise ContractViolation("the pager needs a store with a DeviceKey")
         SlidingWindow(window_capacity)  # validate range up front
         self.store = store
+        self._native_fault = getattr(store, "fault", None)  # DevicePageStore.fault: one call per fault
         self.fetch_evicted = fetch_evicted
         self.window_capacity = window_capacity
         self._windows: dict[object, SlidingWindow] = {}
@@ -139,7 +140,7 @@ class WindowPager:
 
     def fault(self, client, vaddr: int) -> bytes:
         """Resolve one fault (handle_fault, orchestrator.py:175-211)."""
-        return self.fault_batch(client, [vaddr])[0].tobytes()
+        return self._fault_one(client, vaddr)[0].tobytes()
 
     def fault_batch(self, client, vaddrs) -> np.ndarray:
         """Resolve faults on distinct, non-resident pages, in order; returns
@@ -225,9 +226,8 @@ class WindowPager:
             raise ContractViolation(f"vaddr {v:#x} not page-aligned")
         if win.resident(v):
             raise ContractViolation(f"fault on resident page {v:#x}")
-        native = getattr(self.store, "fault", None)
-        if native is not None:
-            return self._fault_one_native(client, win, m, v, native)
+        if self._native_fault is not None:
+            return self._fault_one_native(client, win, m, v, self._native_fault)
         refault = self.store.contains(client, v)
         e = win.admit(v)
         try:
