@@ -85,6 +85,30 @@ class TestDevicePath:
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), r["ct"])
 
+    @pytest.mark.parametrize("shape", ["vaddr_array", "pid_array", "both"])
+    @pytest.mark.parametrize("rounds", [8, 12, 20])
+    @pytest.mark.parametrize("n", [1, 2, 3, 5, 1183, 2369, 4097])
+    def test_every_descriptor_shape_ragged(self, dkey, shape, rounds, n):
+        """Each descriptor shape compiles to its own loop (DM = vaddr array |
+        pid array; page-pair loops for R <= 12 and for R = 20 with a vaddr
+        array alone): ragged counts around the grid stride (296 or 444 CTAs
+        x 4 pages), random vaddrs whose high word changes page to page,
+        vaddrs crossing 4 GiB, random u32 pids."""
+        import torch
+
+        rng = np.random.default_rng(n * 31 + rounds)
+        pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
+        va = (rng.integers(0, 2**52, size=n, dtype=np.uint64) << np.uint64(12))
+        va[: n // 2] = 0xFFFF_F000 + 4096 * np.arange(n // 2, dtype=np.uint64)  # crosses 4 GiB
+        pi = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        v_arg = t(va.view(np.int64)) if shape != "pid_array" else BASE
+        p_arg = t(pi.view(np.int32)) if shape != "vaddr_array" else 77
+        v_ref = va if shape != "pid_array" else BASE + 4096 * np.arange(n, dtype=np.uint64)
+        p_ref = pi if shape != "vaddr_array" else np.full(n, 77, np.uint32)
+        got = pc.crypt_pages(dkey, v_arg, p_arg, t(pages), rounds=rounds)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=rounds, nthreads=8))
+
     @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5])
     def test_pid_per_page_variant(self, dkey, kernel, knob):
         """pid = 1 + (i % 64); also vaddr_hi changing mid-batch
