@@ -1,3 +1,5 @@
+"""Diagnostic: 1-page service latency (bare ctypes pc_service_crypt, p50)
+before and after other library/torch state is created in the process."""
 import os, sys, time, ctypes
 sys.path.insert(0, os.getcwd())
 import torch

@@ -1,3 +1,6 @@
+"""1-page service latency (bare ctypes pc_service_crypt, p50) against the
+worker count (1, 8, 16, 148) and the worker a client routes to
+(profiles/r01_service_workers_probe.txt)."""
 import os, sys, time, ctypes
 sys.path.insert(0, os.getcwd())
 import paper_2004_09252_b200 as pc
