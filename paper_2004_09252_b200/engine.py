@@ -315,6 +315,12 @@ def crypt_pages(key, vaddrs, pids, pages, *, rounds: int = 20, out=None, stream=
             torch CPU tensor / buffer; synchronous, via the engine's pipeline).
     out     destination of the same kind; defaults to a new buffer.  ``out``
             may be ``pages`` (in place).
+    check   device path with a CUDA vaddr tensor: validate page alignment
+            on the device first (ContractViolation at call time, as the
+            reference raises).  The check synchronises ``stream``; pass
+            False to keep the call fully asynchronous when the descriptors
+            are known good.  (An int64 pid tensor is always narrowed and
+            range-checked by the same library kernel.)
     Returns ``out``.
     """
     _check_rounds(rounds)
