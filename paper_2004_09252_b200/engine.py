@@ -319,8 +319,9 @@ def crypt_pages(key, vaddrs, pids, pages, *, rounds: int = 20, out=None, stream=
             on the device first (ContractViolation at call time, as the
             reference raises).  The check synchronises ``stream``; pass
             False to keep the call fully asynchronous when the descriptors
-            are known good.  (An int64 pid tensor is always narrowed and
-            range-checked by the same library kernel.)
+            are known good.  (An int64 pid tensor is always narrowed to
+            u32 by the same library kernel, which also synchronises; its
+            range check raises only when ``check`` is True.)
     Returns ``out``.
     """
     _check_rounds(rounds)
