@@ -541,6 +541,7 @@ struct pc_key {
   cudaStream_t kst;      // key's private stream: depends on every device-path use
   cudaEvent_t ev;
   std::mutex mu;
+  std::atomic<int> refs{0}; // stores holding this key; destroy refuses while > 0
 };
 
 namespace {
@@ -710,6 +711,8 @@ int pc_key_generate(int device, const uint8_t entropy[32], pc_key **out) {
 int pc_key_destroy(pc_key *key) {
   if (!key) return PC_OK;
   if (key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  if (const int r = key->refs.load())
+    return fail(PC_ESTATE, "key is still held by %d page store(s); destroy them first", r);
   DeviceGuard g(key->device);
   CU(g.err);
   {
@@ -946,7 +949,7 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
     // ramp: powers of two from 1024 pages (4 MiB) up to C/2, so the first
     // transfer is small whatever the steady-state chunk is
     std::vector<size_t> ramp;
-    for (size_t r = std::min<size_t>(1024, C / 8); r < C; r *= 2) ramp.push_back(r);
+    for (size_t r = std::max<size_t>(1, std::min<size_t>(1024, C / 8)); r < C; r *= 2) ramp.push_back(r);
     size_t ramp_sum = 0;
     for (size_t r : ramp) ramp_sum += r;
     const bool do_ramp = C >= 64 && n >= 2 * ramp_sum + 2 * C;
@@ -1149,9 +1152,12 @@ extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, siz
     uint8_t *h = e->h_small;
     uint8_t *hd = e->hd_small;
     std::memcpy(h, slots, n * 4);
+    // staging layout: slots [0,256) | vaddrs [256,768) | pids [768,1024) | pages
     if (key && vaddrs) std::memcpy(h + 256, vaddrs, n * 8);
+    if (key && pids) std::memcpy(h + 768, pids, n * 4);
     if (dir == 0) std::memcpy(h + 1024, host, n * PC_PAGE_SIZE);
-    const pc::PageDesc d{key && vaddrs ? reinterpret_cast<const uint64_t *>(hd + 256) : nullptr, nullptr, vaddr0, pid0};
+    const pc::PageDesc d{key && vaddrs ? reinterpret_cast<const uint64_t *>(hd + 256) : nullptr,
+                         key && pids ? reinterpret_cast<const uint32_t *>(hd + 768) : nullptr, vaddr0, pid0};
     const uint32_t *k = key ? key->d_words : nullptr;
     cudaStream_t st = e->streams[0];
     switch (rounds) {
@@ -1280,7 +1286,10 @@ int pc_desc_check(const uint64_t *vaddrs, const int64_t *pids64, uint32_t *pids3
   if (pids64 && !pids32) return fail(PC_EINVAL, "pids32 is NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int dev = 0;
-  CU(cudaGetDevice(&dev));
+  // the launch must run on the stream's own device, whatever is current
+  CU(st ? cudaStreamGetDevice(st, &dev) : cudaGetDevice(&dev));
+  DeviceGuard g(dev);
+  CU(g.err);
   Scratch &sc = scratch(dev);
   std::lock_guard<std::mutex> lk(sc.mu);
   int rc = scratch_reserve(sc, 256);

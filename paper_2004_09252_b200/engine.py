@@ -142,8 +142,9 @@ class DeviceKey:
     def destroy(self) -> None:
         """Zero the device copy and free it (workers.py:252-254).  Idempotent."""
         if self._handle is not None:
-            h, self._handle = self._handle, None
-            _native.call("pc_key_destroy", h)
+            # a key still held by a page store is refused (PC_ESTATE) and stays live
+            _native.call("pc_key_destroy", self._handle)
+            self._handle = None
 
     def __enter__(self) -> "DeviceKey":
         return self

@@ -105,6 +105,9 @@ def crypt_pages_multi(keys: list[DeviceKey], engines: list[Engine], vaddrs, pids
         n = arr.shape[0]
         if out is None:
             out = np.empty_like(arr)
+        elif not (isinstance(out, np.ndarray) and out.dtype == np.uint8 and out.flags.c_contiguous
+                  and out.flags.writeable and out.nbytes == n * PAGE_SIZE):
+            raise ContractViolation("out must be a writable C-contiguous uint8 array of n*4096 bytes")
         src, dst = arr.ctypes.data, out.ctypes.data
     v_arr, vaddr0 = _host_vaddrs(vaddrs, n)
     p_arr, pid0 = _host_pids(pids, n)
