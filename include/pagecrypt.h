@@ -83,8 +83,27 @@ int pc_keystream_raw(const uint8_t key[32], const uint8_t *seeds16, size_t k,
  * host RAM.  pc_key_destroy zeroes the device copy before freeing it. */
 int pc_key_install(int device, const uint8_t key[32], pc_key **out);
 int pc_key_generate(int device, const uint8_t entropy[32], pc_key **out);
-int pc_key_destroy(pc_key *key);
+int pc_key_destroy(pc_key *key);  /* PC_ESTATE while a page store holds the key */
 int pc_key_device(const pc_key *key, int *device);
+
+/* Key replication across GPUs: the analog of copying the staged key into
+ * every worker's private slot (pkg/src/pagecrypt/workers.py:193-194), with
+ * the copy never passing through host RAM.
+ *   pc_key_replicate: same process, device-to-device (cudaMemcpyPeer over
+ *     NVLink; PC_ESTATE when `device` has no peer access to the source, since
+ *     the driver would otherwise stage the copy through host memory).
+ *   pc_key_export / pc_key_import: one process per GPU (torchrun).  export
+ *     copies the key into a device buffer and returns its 64-byte CUDA-IPC
+ *     handle (an opaque name of device memory, not key material); import, in
+ *     another process, maps that buffer and copies the 32 bytes device-to-
+ *     device into a new key on `device`.  The exporter keeps the export open
+ *     until every importer has returned, then pc_key_export_close zeroes it
+ *     (destroy closes it too). */
+#define PC_KEY_HANDLE_SIZE 64
+int pc_key_replicate(const pc_key *src, int device, pc_key **out);
+int pc_key_export(pc_key *key, uint8_t handle[PC_KEY_HANDLE_SIZE]);
+int pc_key_export_close(pc_key *key);
+int pc_key_import(int device, const uint8_t handle[PC_KEY_HANDLE_SIZE], pc_key **out);
 
 /* ---- (iv) device-resident batch ----------------------------------------
  * The batched form of cipher.crypt_page (pkg/src/pagecrypt/cipher.py:205-217)
@@ -118,6 +137,11 @@ int pc_desc_check(const uint64_t *vaddrs, const int64_t *pids64, uint32_t *pids3
  * slot for this call and zeroes it before returning). */
 int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **out);
 int pc_engine_destroy(pc_engine *eng);
+/* Host placement chosen for the engine: the NUMA node of the
+ * GPU's PCIe root (-1 = not reported) and how many GPU-local CPUs its runner
+ * and bounce threads are bound to (0 = unbound).  Pinned staging is
+ * allocated on that node. */
+int pc_engine_placement(const pc_engine *eng, int *numa_node, int *n_cpus);
 int pc_crypt_pages_host(pc_engine *eng, const pc_key *key, const uint8_t *raw_key,
                         const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
                         uint32_t pid0, const void *in, void *out, size_t n, int rounds);

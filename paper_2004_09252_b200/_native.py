@@ -40,11 +40,16 @@ SIGNATURES = {
     "pc_key_generate": (c_int, [c_int, c_void_p, P(c_void_p)]),
     "pc_key_destroy": (c_int, [c_void_p]),
     "pc_key_device": (c_int, [c_void_p, P(c_int)]),
+    "pc_key_replicate": (c_int, [c_void_p, c_int, P(c_void_p)]),
+    "pc_key_export": (c_int, [c_void_p, c_void_p]),
+    "pc_key_export_close": (c_int, [c_void_p]),
+    "pc_key_import": (c_int, [c_int, c_void_p, P(c_void_p)]),
     "pc_crypt_pages_dev": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, c_u32, c_void_p, c_void_p,
                                    c_size_t, c_int, c_void_p]),
     "pc_desc_check": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, P(c_u32)]),
     "pc_engine_create": (c_int, [c_int, c_int, c_size_t, P(c_void_p)]),
     "pc_engine_destroy": (c_int, [c_void_p]),
+    "pc_engine_placement": (c_int, [c_void_p, P(c_int), P(c_int)]),
     "pc_crypt_pages_host": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_u64, c_u32,
                                     c_void_p, c_void_p, c_size_t, c_int]),
     "pc_crypt_pages_multi": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_u64, c_u32,

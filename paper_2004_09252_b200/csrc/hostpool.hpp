@@ -13,12 +13,18 @@
 #include <thread>
 #include <vector>
 
+#include "numa.hpp"
+
 namespace pc {
 
 class HostPool {
  public:
-  explicit HostPool(unsigned n) {
-    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  // Threads run on the GPU-local CPUs of `where` (see numa.hpp).
+  explicit HostPool(unsigned n, const DevicePlacement &where = DevicePlacement()) {
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this, where] {
+      bind_thread(where);
+      loop();
+    });
   }
   ~HostPool() {
     {
@@ -114,7 +120,10 @@ class HostPool {
 // (measured at ~40 ms per new thread on the B200 host).
 class Runner {
  public:
-  Runner() : t_([this] { loop(); }) {}
+  explicit Runner(const DevicePlacement &where = DevicePlacement()) : t_([this, where] {
+    bind_thread(where);
+    loop();
+  }) {}
   ~Runner() {
     {
       std::lock_guard<std::mutex> lk(mu_);

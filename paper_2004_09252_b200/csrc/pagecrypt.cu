@@ -383,14 +383,23 @@ bool device_memory(const void *p, int *device) {
   return true;
 }
 
+// Persistent services running per device (pc_service_start/stop).
+std::atomic<int> g_services_on[64];
+bool service_running(int d) { return d >= 0 && d < 64 && g_services_on[d].load() > 0; }
+
 // Can kernels on `dev` load/store `peer`'s memory?  Enables peer access once
 // per (dev, peer) pair and caches the answer (NVSwitch: every pair can).
+// Enabling is never attempted while a persistent service runs on either
+// device (the enable may wait for that device to idle): the answer is then
+// "no" for now, and callers take their staged-copy paths.  pc_service_start
+// enables the pairs it can see before it launches, so this is the rare case.
 bool peer_access(int dev, int peer) {
   static std::mutex mu;
   static std::map<std::pair<int, int>, bool> known;
   std::lock_guard<std::mutex> lk(mu);
   auto it = known.find({dev, peer});
   if (it != known.end()) return it->second;
+  if (service_running(dev) || service_running(peer)) return false; // not cached: retried later
   int can = 0;
   bool ok = cudaDeviceCanAccessPeer(&can, dev, peer) == cudaSuccess && can;
   if (ok) {
@@ -542,6 +551,7 @@ struct pc_key {
   cudaEvent_t ev;
   std::mutex mu;
   std::atomic<int> refs{0}; // stores holding this key; destroy refuses while > 0
+  void *ipc_buf = nullptr;  // live CUDA-IPC export of the key (pc_key_export), or NULL
 };
 
 namespace {
@@ -554,6 +564,38 @@ int note_key_use(pc_key *key, cudaStream_t st) {
   return PC_OK;
 }
 
+// Free a key object's device slot (zeroed first), stream and event.
+void key_free(pc_key *k) {
+  if (k->d_words) {
+    cudaMemsetAsync(k->d_words, 0, 256, k->kst);
+    cudaFreeAsync(k->d_words, k->kst);
+    cudaStreamSynchronize(k->kst);
+  }
+  if (k->ev) cudaEventDestroy(k->ev);
+  if (k->kst) cudaStreamDestroy(k->kst);
+  k->magic = 0;
+  delete k;
+}
+
+// An empty key object on `device` (current device must be `device`): its
+// private stream and event and a zeroed 256-byte stream-ordered slot.
+int key_new(int device, pc_key **out) {
+  *out = nullptr;
+  auto *k = new pc_key();
+  k->magic = kKeyMagic;
+  k->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&k->kst, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&k->ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void **>(&k->d_words), 256, k->kst);
+  if (e == cudaSuccess) e = cudaMemsetAsync(k->d_words, 0, 256, k->kst);
+  if (e != cudaSuccess) {
+    key_free(k);
+    return fail(e == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA, "key slot: %s", cudaGetErrorString(e));
+  }
+  *out = k;
+  return PC_OK;
+}
+
 // Allocate a key object on `device` and fill its 32 bytes from `src` through
 // the pinned scratch (wiped afterwards).  If `derive`, src is entropy and the
 // key is derived on the device by k_keygen.
@@ -561,37 +603,22 @@ int key_create(int device, const uint8_t *src, bool derive, pc_key **out) {
   *out = nullptr;
   DeviceGuard g(device);
   CU(g.err);
-  auto *k = new pc_key();
-  k->magic = kKeyMagic;
-  k->device = device;
-  auto bail = [&](int rc) {
-    if (k->d_words) {
-      cudaMemsetAsync(k->d_words, 0, 256, k->kst);
-      cudaFreeAsync(k->d_words, k->kst);
-      cudaStreamSynchronize(k->kst);
-    }
-    if (k->ev) cudaEventDestroy(k->ev);
-    if (k->kst) cudaStreamDestroy(k->kst);
-    delete k;
-    return rc;
-  };
-#define CUK(call)                                                                       \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess) return bail(fail(PC_ECUDA, "%s: %s", #call, cudaGetErrorString(e_))); \
-  } while (0)
-  CUK(cudaStreamCreateWithFlags(&k->kst, cudaStreamNonBlocking));
-  CUK(cudaEventCreateWithFlags(&k->ev, cudaEventDisableTiming));
-  CUK(cudaMallocAsync(reinterpret_cast<void **>(&k->d_words), 256, k->kst));
+  pc_key *k = nullptr;
+  int rc = key_new(device, &k);
+  if (rc != PC_OK) return rc;
+  cudaError_t e;
   {
     Scratch &sc = scratch(device);
     std::lock_guard<std::mutex> lk(sc.mu);
-    int rc = scratch_reserve(sc, 256);
-    if (rc != PC_OK) return bail(rc);
+    rc = scratch_reserve(sc, 256);
+    if (rc != PC_OK) {
+      key_free(k);
+      return rc;
+    }
     std::memcpy(sc.h, src, 32);
     // key (or entropy) lands at d_words[0..7] / d_words[8..15]
     uint32_t *dst = derive ? k->d_words + 8 : k->d_words;
-    cudaError_t e = cudaMemcpyAsync(dst, sc.h, 32, cudaMemcpyHostToDevice, k->kst);
+    e = cudaMemcpyAsync(dst, sc.h, 32, cudaMemcpyHostToDevice, k->kst);
     if (e == cudaSuccess && derive) {
       pc::k_keygen<<<1, 1, 0, k->kst>>>(k->d_words + 8, k->d_words);
       counted();
@@ -601,11 +628,26 @@ int key_create(int device, const uint8_t *src, bool derive, pc_key **out) {
     cudaError_t e2 = cudaStreamSynchronize(k->kst);
     wipe(sc.h, 32);
     if (e == cudaSuccess) e = e2;
-    CUK(e);
   }
-#undef CUK
+  if (e != cudaSuccess) {
+    key_free(k);
+    return fail(PC_ECUDA, "key install: %s", cudaGetErrorString(e));
+  }
   *out = k;
   return PC_OK;
+}
+
+// CUDA-IPC export buffers (cudaMalloc'd: IPC handles cannot name
+// stream-ordered pool memory).  cudaFree synchronises the device, which never
+// returns while a persistent service runs, so closed exports are zeroed and
+// recycled here instead of freed.
+struct ExportPool {
+  std::mutex mu;
+  std::map<int, std::vector<void *>> free; // device -> zeroed 256-byte buffers
+};
+ExportPool &export_pool() {
+  static ExportPool *p = new ExportPool(); // intentionally never destroyed
+  return *p;
 }
 } // namespace
 
@@ -634,6 +676,7 @@ struct pc_engine {
   std::unique_ptr<pc::HostPool> pool; // pageable <-> pinned bounce copies (lazy)
   std::unique_ptr<pc::Runner> runner; // this engine's thread for multi-device calls (lazy)
   std::mutex runner_mu;
+  pc::DevicePlacement place;          // GPU-local CPUs / NUMA node for threads and pinned staging
 };
 
 // ===========================================================================
@@ -715,6 +758,10 @@ int pc_key_destroy(pc_key *key) {
     return fail(PC_ESTATE, "key is still held by %d page store(s); destroy them first", r);
   DeviceGuard g(key->device);
   CU(g.err);
+  if (key->ipc_buf) {
+    int rc = pc_key_export_close(key);
+    if (rc != PC_OK) return rc;
+  }
   {
     std::lock_guard<std::mutex> lk(key->mu);
     // kst already waits for every device-path use of the key (note_key_use)
@@ -734,6 +781,129 @@ int pc_key_device(const pc_key *key, int *device) {
   if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
   if (!device) return fail(PC_EINVAL, "device is NULL");
   *device = key->device;
+  return PC_OK;
+}
+
+
+// ---- key replication (the key replicated into each device) -----
+int pc_key_replicate(const pc_key *src, int device, pc_key **out) {
+  if (!out) return fail(PC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!src || src->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(PC_EINVAL, "device %d outside 0..%d", device, ndev - 1);
+  // a cross-device copy without peer access would be staged by the driver
+  // through host memory: refuse rather than let the key touch host RAM
+  if (device != src->device && !peer_access(device, src->device))
+    return fail(PC_ESTATE, "no peer access from device %d to device %d: the key cannot be copied "
+                "device-to-device", device, src->device);
+  DeviceGuard g(device);
+  CU(g.err);
+  pc_key *k = nullptr;
+  int rc = key_new(device, &k);
+  if (rc != PC_OK) return rc;
+  cudaError_t e = cudaMemcpyPeerAsync(k->d_words, device, src->d_words, src->device, 32, k->kst);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(k->kst);
+  if (e != cudaSuccess) {
+    key_free(k);
+    return fail(PC_ECUDA, "key replicate: %s", cudaGetErrorString(e));
+  }
+  *out = k;
+  return PC_OK;
+}
+
+int pc_key_export(pc_key *key, uint8_t handle[PC_KEY_HANDLE_SIZE]) {
+  if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  if (!handle) return fail(PC_EINVAL, "handle is NULL");
+  static_assert(sizeof(cudaIpcMemHandle_t) == PC_KEY_HANDLE_SIZE, "IPC handle size");
+  DeviceGuard g(key->device);
+  CU(g.err);
+  std::lock_guard<std::mutex> lk(key->mu);
+  if (!key->ipc_buf) {
+    void *buf = nullptr;
+    {
+      ExportPool &xp = export_pool();
+      std::lock_guard<std::mutex> l2(xp.mu);
+      auto &v = xp.free[key->device];
+      if (!v.empty()) {
+        buf = v.back();
+        v.pop_back();
+      }
+    }
+    if (!buf) {
+      cudaError_t e = cudaMalloc(&buf, 256);
+      if (e != cudaSuccess) return fail(PC_ENOMEM, "export buffer: %s", cudaGetErrorString(e));
+    }
+    cudaError_t e = cudaMemcpyAsync(buf, key->d_words, 32, cudaMemcpyDeviceToDevice, key->kst);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(key->kst);
+    if (e != cudaSuccess) {
+      std::lock_guard<std::mutex> l2(export_pool().mu);
+      export_pool().free[key->device].push_back(buf);
+      return fail(PC_ECUDA, "key export: %s", cudaGetErrorString(e));
+    }
+    key->ipc_buf = buf;
+  }
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, key->ipc_buf));
+  std::memcpy(handle, &h, sizeof h);
+  return PC_OK;
+}
+
+int pc_key_export_close(pc_key *key) {
+  if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  DeviceGuard g(key->device);
+  CU(g.err);
+  std::lock_guard<std::mutex> lk(key->mu);
+  if (!key->ipc_buf) return PC_OK;
+  cudaError_t e = cudaMemsetAsync(key->ipc_buf, 0, 256, key->kst);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(key->kst);
+  CU(e);
+  {
+    std::lock_guard<std::mutex> l2(export_pool().mu);
+    export_pool().free[key->device].push_back(key->ipc_buf);
+  }
+  key->ipc_buf = nullptr;
+  return PC_OK;
+}
+
+int pc_key_import(int device, const uint8_t handle[PC_KEY_HANDLE_SIZE], pc_key **out) {
+  if (!out) return fail(PC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!handle) return fail(PC_EINVAL, "handle is NULL");
+  DeviceGuard g(device);
+  CU(g.err);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void *peer = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&peer, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PC_ECUDA, "cudaIpcOpenMemHandle: %s (the exporting process must be alive, its export "
+                "open, and this device able to reach the exporter's device)", cudaGetErrorString(e));
+  }
+  pc_key *k = nullptr;
+  int rc = key_new(device, &k);
+  if (rc == PC_OK) {
+    // device-to-device (same GPU, or NVLink peer read of the exporter's GPU)
+    e = cudaMemcpyAsync(k->d_words, peer, 32, cudaMemcpyDeviceToDevice, k->kst);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(k->kst);
+    if (e != cudaSuccess) {
+      key_free(k);
+      k = nullptr;
+      rc = fail(PC_ECUDA, "key import: %s", cudaGetErrorString(e));
+    }
+  }
+  cudaIpcCloseMemHandle(peer);
+  *out = k;
+  return rc;
+}
+
+int pc_engine_placement(const pc_engine *e, int *numa_node, int *n_cpus) {
+  if (!e || e->magic != kEngineMagic) return fail(PC_ESTATE, "not a live pc_engine");
+  if (!numa_node || !n_cpus) return fail(PC_EINVAL, "NULL output");
+  *numa_node = e->place.node;
+  *n_cpus = e->place.has_cpus ? CPU_COUNT(&e->place.cpus) : 0;
   return PC_OK;
 }
 
@@ -772,6 +942,8 @@ int pc_engine_create(int device, int n_streams, size_t chunk_pages, pc_engine **
   e->device = device;
   e->n_streams = n_streams;
   e->chunk_pages = chunk_pages;
+  e->place = pc::device_placement(device);
+  pc::NodeScope near_gpu(e->place); // pinned staging below is first touched on the GPU's node
   auto cleanup = [&](int rc) {
     pc_engine_destroy(e);
     return rc;
@@ -935,9 +1107,10 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
   // caller's pinned output over PCIe (posted writes), so no D2H copy runs
   const bool direct_out = hm == 3 && out_dev && dedicated;
   if (!pin_in || !pin_out) {
+    pc::NodeScope near_gpu(e->place);
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
-    if (!e->pool) e->pool.reset(new pc::HostPool(host_pool_threads()));
+    if (!e->pool) e->pool.reset(new pc::HostPool(host_pool_threads(), e->place));
   }
   // Chunk schedule: ramp up C/8, C/4, C/2 at the start and down at the end
   // (when the batch is large enough) so the pipeline fills and drains with
@@ -1178,9 +1351,10 @@ extern "C" int pc_slab_transfer(pc_engine *e, const pc_key *key, void *slab, siz
   const int S = e->n_streams;
   const size_t C = e->chunk_pages;
   if (!pinned) {
+    pc::NodeScope near_gpu(e->place);
     for (int s = 0; s < S; ++s)
       if (!e->h_bounce[s]) CU(pinned_get(reinterpret_cast<void **>(&e->h_bounce[s]), C * PC_PAGE_SIZE));
-    if (!e->pool) e->pool.reset(new pc::HostPool(host_pool_threads()));
+    if (!e->pool) e->pool.reset(new pc::HostPool(host_pool_threads(), e->place));
   }
   auto *hb = static_cast<uint8_t *>(host);
   const size_t n_chunks = (n + C - 1) / C;
@@ -1335,7 +1509,7 @@ int pc_crypt_pages_multi(pc_engine *const *engines, const pc_key *const *keys, i
     pc_engine *e = engines[g];
     {
       std::lock_guard<std::mutex> lk(e->runner_mu);
-      if (!e->runner) e->runner.reset(new pc::Runner());
+      if (!e->runner) e->runner.reset(new pc::Runner(e->place));
     }
     waits.push_back(e->runner->submit([&job, g] { job(g); }));
   }
@@ -1427,6 +1601,34 @@ int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key
   return PC_OK;
 }
 
+// Enable peer access both ways between `dev` and every GPU this process
+// already has a context on (a device with no context is left alone: creating
+// contexts on every GPU of the node from every rank would cost HBM on each).
+void enable_peers_of(int dev) {
+  using GetState = int (*)(int, unsigned *, int *);
+  static GetState get_state = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuDevicePrimaryCtxGetState", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<GetState>(f);
+  }();
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || !get_state) {
+    cudaGetLastError();
+    return;
+  }
+  for (int p = 0; p < n; ++p) {
+    if (p == dev) continue;
+    unsigned flags = 0;
+    int active = 0;
+    if (get_state(p, &flags, &active) != 0 || !active) continue; // CUdevice == ordinal
+    peer_access(dev, p);
+    peer_access(p, dev);
+  }
+}
+
 inline void cpu_relax() {
 #if defined(__x86_64__)
   __builtin_ia32_pause();
@@ -1490,6 +1692,7 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
   CU(g.err);
   rc = pc_preload(key->device); // nothing of ours may lazy-load behind the service
   if (rc != PC_OK) return rc;
+  enable_peers_of(key->device); // no peer-access enable has to happen beside the kernel
   auto *s = new pc_service();
   s->device = key->device;
   s->n_workers = n_workers;
@@ -1564,6 +1767,7 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
       std::this_thread::yield();
     }
   }
+  g_services_on[s->device].fetch_add(1);
   *out = s;
   return PC_OK;
 }
@@ -1711,6 +1915,7 @@ int pc_service_stop(pc_service *s) {
   s->stopped = true;
   *reinterpret_cast<volatile uint32_t *>(s->h_ctrl) = 1;
   cudaError_t e = cudaStreamSynchronize(s->st);
+  g_services_on[s->device].fetch_sub(1);
   const size_t nslots = static_cast<size_t>(s->n_workers) * s->ring;
   wipe(s->h_pages, nslots * PC_PAGE_SIZE);
   cudaFreeAsync(s->dev, s->st);

@@ -125,6 +125,39 @@ class DeviceKey:
             del buf
         return cls(h.value, device)
 
+    def replicate(self, device: int) -> "DeviceKey":
+        """The same key on another GPU, copied device-to-device (NVLink peer
+        copy; refused rather than staged through host RAM when the GPUs have
+        no peer access).  The analog of the per-worker key slots filled from
+        one staged key (workers.py:193-194)."""
+        h = ctypes.c_void_p()
+        _native.call("pc_key_replicate", self.handle, int(device), ctypes.byref(h))
+        return DeviceKey(h.value, int(device))
+
+    def export_handle(self) -> bytes:
+        """64-byte CUDA-IPC handle of a device copy of the key, for
+        :meth:`import_handle` in another process (one process per GPU).  The
+        handle names device memory; it is not key material.  Keep the export
+        open until every importer has returned, then :meth:`close_export`."""
+        buf = (ctypes.c_uint8 * 64)()
+        _native.call("pc_key_export", self.handle, buf)
+        return bytes(buf)
+
+    def close_export(self) -> None:
+        """Zero the exported copy (importers already hold their own keys)."""
+        _native.call("pc_key_export_close", self.handle)
+
+    @classmethod
+    def import_handle(cls, handle: bytes, device: int = 0) -> "DeviceKey":
+        """A key on ``device`` copied device-to-device from another process's
+        :meth:`export_handle` (the exporter must keep its export open)."""
+        if len(handle) != 64:
+            raise ContractViolation("key handle must be 64 bytes")
+        buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+        h = ctypes.c_void_p()
+        _native.call("pc_key_import", int(device), buf, ctypes.byref(h))
+        return cls(h.value, int(device))
+
     @property
     def device(self) -> int:
         return self._device
@@ -180,6 +213,14 @@ class Engine:
         if self._handle is not None:
             h, self._handle = self._handle, None
             _native.call("pc_engine_destroy", h)
+
+    @property
+    def placement(self) -> dict:
+        """Host placement of the engine's threads and pinned staging: the
+        GPU's NUMA node (-1 = not reported) and the GPU-local CPUs bound."""
+        node, ncpu = ctypes.c_int(), ctypes.c_int()
+        _native.call("pc_engine_placement", self.handle, ctypes.byref(node), ctypes.byref(ncpu))
+        return {"numa_node": node.value, "bound_cpus": ncpu.value}
 
     def __del__(self):
         try:

@@ -119,3 +119,41 @@ def crypt_pages_multi(keys: list[DeviceKey], engines: list[Engine], vaddrs, pids
                  None if p_arr is None else p_arr.ctypes.data,
                  vaddr0, pid0, src, dst, n, rounds)
     return out
+
+
+def replicated_keys(key: DeviceKey, devices: list[int]) -> list[DeviceKey]:
+    """One key per device for :func:`crypt_pages_multi`: ``key`` itself on
+    its own device, device-to-device replicas elsewhere (never via host RAM;
+    workers.py:193-194 fills every worker slot from one staged key)."""
+    return [key if d == key.device else key.replicate(d) for d in devices]
+
+
+def shared_key(device: int, *, group=None, src: int = 0) -> DeviceKey:
+    """One production key shared by every rank of the default process group
+    (one process per GPU).  Rank ``src`` derives it on its GPU
+    (DeviceKey.generate: never in host RAM) and exports a CUDA-IPC handle of a
+    device copy; the handle (an opaque name of device memory, not key
+    material) is broadcast, every other rank copies the key device-to-device
+    onto ``device``, and after a barrier the exporter zeroes its export.
+    Collective: every rank must call it.  Without an initialised process
+    group it is DeviceKey.generate(device)."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return DeviceKey.generate(device)
+    rank = dist.get_rank(group)
+    key = DeviceKey.generate(device) if rank == src else None
+    box = [key.export_handle() if key is not None else None]
+    dist.broadcast_object_list(box, src=src, group=group)
+    err = None
+    if key is None:
+        try:
+            key = DeviceKey.import_handle(box[0], device)
+        except Exception as exc:  # keep the collective schedule; raise after the barrier
+            err = exc
+    dist.barrier(group=group)
+    if rank == src:
+        key.close_export()
+    if err is not None:
+        raise err
+    return key

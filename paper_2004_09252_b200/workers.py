@@ -157,7 +157,7 @@ class WorkerPool:
             # positive control for the cold-boot key scanner (workers.py:196-200)
             from_ram = getattr(self.ram, "alloc", None)
             if from_ram is not None:
-                leak = self.ram.alloc(getattr(self.ram, "TAG_SERVER_MISC", 1), KEY_SIZE)
+                leak = self.ram.alloc("server_misc", KEY_SIZE)  # TAG_SERVER_MISC (ram.py:29)
                 leak.data[:] = staging
         dkey = DeviceKey.install(staging, self.device)
         staging[:] = bytes(KEY_SIZE)

@@ -28,13 +28,48 @@ def test_reference_arm_line():
     assert d["metric"].startswith("GB/s of pages") and d["unit"] == "GB/s" and d["higher_is_better"] is True
     assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    # the unmodified reference (oracle/_ref snapshot, numba) whenever it is here
+    assert cb["kind"] == ("reference" if _reference_available() else "port")
+    if cb["kind"] == "reference":
+        assert cb["spot_check_ok"] is True
+        assert {"single_thread", "worker_pool", "crypt_page_latency_us"} <= set(cb)
     assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["rounds"] == 20 and d["config"]["pages_per_gpu"] == 262144
 
 
+def _reference_available():
+    sys.path.insert(0, ROOT)
+    from oracle import ref_bench
+
+    return ref_bench.load() is not None
+
+
+def test_self_launch_two_ranks_without_torchrun():
+    """--gpus 2 with no WORLD_SIZE: bench.py starts its own two ranks
+    (torch.distributed.run on 127.0.0.1) and rank 0's line says n_gpus 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "3", "--warmup", "3", "--ref-pages", "256", "--dist-backend", "gloo"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_gpus_must_match_world_size():
+    r = run_bench("--impl", "reference", "--gpus", "2", "--steps", "3", "--warmup", "3", "--ref-pages", "64",
+                  env={"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0"})
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+
+
 def test_reference_arm_other_ranks_are_silent():
     r = run_bench("--impl", "reference", "--steps", "3", "--warmup", "3", "--ref-pages", "64",
+                  env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 2  # --gpus defaults to 1: a mismatched world is refused
+    r = run_bench("--impl", "reference", "--gpus", "2", "--steps", "3", "--warmup", "3", "--ref-pages", "64",
                   env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
