@@ -604,6 +604,165 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
 }
 
 // ---------------------------------------------------------------------------
+// v6: v5's cp.async page ring with the per-page seed rounds computed once
+// per page instead of once per thread.
+//
+// Of the first column round's four quarter rounds, three depend on the page
+// alone: column 0 on vaddr_lo, column 1 on vaddr_hi, column 2 on the pid
+// (state words 12..14); only column 3 holds the block index.  v5 hoists
+// column 3 per thread and caches columns 1/2 while vaddr_hi/pid repeat, but
+// still runs column 0 -- and, with a per-page pid array, column 2 -- in all
+// 64 threads of every page.  Here the 64 threads of a page slot compute those
+// three columns for the slot's next 32 pages together (lane L of each of the
+// slot's two warps takes page 16*half + L, L < 16), file them in a
+// shared-memory table, and every thread then reads its page's entry with
+// four broadcast LDS.128: per page and warp, 4 LDS replace 8-16 instructions
+// on the ALU pipe, the pipe that binds ChaCha12/20.  The descriptor arrays
+// are read once per page (one strided LDG per computing lane, prefetched a
+// batch ahead) instead of once per page per thread.  Every block is still
+// exactly ChaCha_R(state) + state: only common subexpressions are shared.
+constexpr int kV6Stages = 3;
+constexpr int kV6Batch = 32;                                          // pages per table refill
+constexpr size_t kV6RingBytes = kV6Stages * 256 * 4 * 16;              // 48 KiB
+constexpr size_t kV6TableBytes = 4 * kV6Batch * 64;                    // 4 slots x 32 pages x 64 B
+constexpr size_t kV6Smem = kV6RingBytes + kV6TableBytes;               // dynamic shared memory
+
+// The 64 threads of page slot q meet at named barrier 1 + q.  The id is an
+// immediate in each branch: a register id makes ptxas reserve all 16 barriers.
+__device__ __forceinline__ void slot_bar(uint32_t q) {
+  switch (q) {
+    case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+    case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+    case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+    default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+  }
+}
+
+template <int ROUNDS, int DM>
+__global__ void __launch_bounds__(256, 4)
+k_crypt_pages_warp(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
+                   uint32_t n_pages) {
+  constexpr bool VA = (DM & 1) != 0, PA = (DM & 2) != 0;
+  constexpr RotMul rm{};
+  extern __shared__ __align__(16) uint4 v6_smem[];
+  uint4 (*ring)[256 * 4] = reinterpret_cast<uint4 (*)[256 * 4]>(v6_smem);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t q = tid >> 6;               // page slot
+  const uint32_t b = tid & 63;               // block of the page
+  const uint32_t sw = (tid >> 1) & 3;
+  const uint32_t stride = gridDim.x * 4;
+  const uint32_t page0 = blockIdx.x * 4 + q;
+  uint32_t page = page0;
+  if (page >= n_pages) return; // slot-uniform: both warps of the slot leave together
+  uint4 *table = v6_smem + kV6RingBytes / 16 + q * kV6Batch * 4;
+  const uint32_t base0 = smem_u32(&ring[0][tid * 4]);
+  constexpr uint32_t kStageBytes = 256 * 4 * 16;
+  const uint64_t step = static_cast<uint64_t>(stride) * 256; // uint4 per stride
+  const uint4 *src_ahead = in + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint4 *dst = out + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint32_t page_ahead = page;
+  auto issue = [&](int st) {
+    if (page_ahead < n_pages) {
+      const uint32_t sdst = base0 + st * kStageBytes;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async16(sdst + 16 * (c ^ sw), src_ahead + c);
+    }
+    cp_async_commit();
+    page_ahead += stride;
+    src_ahead += step;
+  };
+  issue(0);
+  issue(1);
+  uint32_t k[8];
+  load_key(key, k);
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  // this thread's table entry: page index e = 16*(b >> 5) + (b & 31) for
+  // b & 31 < 16, i.e. page page0 + (32*batch + e)*stride, descriptor
+  // fetched one batch ahead
+  const uint32_t lane = b & 31;
+  const bool filler = lane < 16;
+  const uint32_t e_idx = 16 * (b >> 5) + lane;
+  uint64_t lp = static_cast<uint64_t>(page0) + static_cast<uint64_t>(e_idx) * stride;
+  const uint64_t batch_step = static_cast<uint64_t>(kV6Batch) * stride;
+  uint64_t nv = 0;
+  uint32_t npid = desc.pid0;
+  auto fetch = [&]() {
+    if constexpr (VA) {
+      if (filler && lp < n_pages) nv = __ldg(desc.vaddrs + lp);
+    } else {
+      nv = desc.vaddr0 + (lp << 12);
+    }
+    if constexpr (PA) {
+      if (filler && lp < n_pages) npid = __ldg(desc.pids + lp);
+    }
+  };
+  fetch();
+  auto refill = [&]() {
+    slot_bar(q); // both warps of the slot are done with the previous batch
+    if (filler) {
+      const uint32_t vlo = static_cast<uint32_t>(nv), vhi = static_cast<uint32_t>(nv >> 32), pid = npid;
+      uint32_t a0 = kSigma0, b0 = k[0], e0 = k[4], d0 = vlo;
+      uint32_t a1 = kSigma1, b1 = k[1], e1 = k[5], d1 = vhi;
+      uint32_t a2 = kSigma2, b2 = k[2], e2 = k[6], d2 = pid;
+      quarter_round<0>(a0, b0, e0, d0, rm);
+      quarter_round<0>(a1, b1, e1, d1, rm);
+      quarter_round<0>(a2, b2, e2, d2, rm);
+      table[e_idx * 4 + 0] = make_uint4(a0, b0, e0, d0);
+      table[e_idx * 4 + 1] = make_uint4(a1, b1, e1, d1);
+      table[e_idx * 4 + 2] = make_uint4(a2, b2, e2, d2);
+      table[e_idx * 4 + 3] = make_uint4(vlo, vhi, pid, 0u);
+      lp += batch_step;
+      fetch();
+    }
+    slot_bar(q); // the batch is filed
+  };
+  // the table entry of the NEXT page is loaded while this page's rounds run
+  // (its shared-memory latency stalled the rounds otherwise: ncu
+  // short_scoreboard); the refill for pages 32(B+1).. runs in iteration 32B+31
+  // before that prefetch
+  refill();
+  uint4 q0 = table[0], q1 = table[1], q2 = table[2], sd = table[3];
+  int st = 0;
+  for (uint32_t j = 0;; ++j) {
+    issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
+    uint32_t x[16];
+    x[0] = q0.x; x[4] = q0.y; x[8] = q0.z; x[12] = q0.w;
+    x[1] = q1.x; x[5] = q1.y; x[9] = q1.z; x[13] = q1.w;
+    x[2] = q2.x; x[6] = q2.y; x[10] = q2.z; x[14] = q2.w;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    const uint32_t s0 = sd.x, s1 = sd.y, s2 = sd.z;
+    if (((j + 1) & (kV6Batch - 1)) == 0) refill();
+    {
+      const uint4 *ent = table + ((j + 1) & (kV6Batch - 1)) * 4;
+      q0 = ent[0]; q1 = ent[1]; q2 = ent[2]; sd = ent[3];
+    }
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int r = 1; r < ROUNDS / 2; ++r) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    cp_async_wait<2>(); // this page's group has landed
+    const uint4 *mine = &ring[st][tid * 4];
+    const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s0), d3.y ^ (x[13] + s1), d3.z ^ (x[14] + s2),
+                              d3.w ^ (x[15] + b)));
+    page += stride;
+    if (page >= n_pages) break;
+    dst += step;
+    st = st == 2 ? 0 : st + 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // Slab moves for the HBM page store: page i of a staging batch <-> slot
 // slots[i] of a device slab, optionally through the cipher (key != nullptr).
 // DIR 0: staging -> slab (evict/insert), DIR 1: slab -> staging (refault/lookup).

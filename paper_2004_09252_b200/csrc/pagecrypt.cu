@@ -88,7 +88,8 @@ struct Tuning {
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
   std::atomic<int> kernel{0};          // HBM kernel: 0 = auto (per rounds, below), 1 = k_crypt_blocks,
                                        // 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced,
-                                       // 4 = k_crypt_pages_tma, 5 = k_crypt_pages_async
+                                       // 4 = k_crypt_pages_tma, 5 = k_crypt_pages_async,
+                                       // 6 = k_crypt_pages_warp
   std::atomic<int> host_mode{2};       // large host batches: 0 = round-robin streams, 1 = zero-copy kernel
                                        // (pinned I/O only), 2 = dedicated H2D/compute/D2H streams,
                                        // 3 = as 2 but the kernel writes pinned output directly
@@ -180,7 +181,23 @@ cudaError_t cached_geometry(std::atomic<uint32_t> (&cache)[64], int dev, int &n_
 
 // Persistent grid for k_crypt_pages: SMs x resident CTAs (occupancy), capped
 // by the number of 4-page slots.
-template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async
+// v6 needs more than the 48 KiB static limit of dynamic shared memory: opt
+// each instantiation in once per device.
+template <int R, int DM>
+cudaError_t v6_opt_in() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(pc::k_crypt_pages_warp<R, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(pc::kV6Smem));
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async, 3 = v6 warp-shared seeds
 unsigned pages_grid(size_t n_pages) {
   static std::atomic<uint32_t> geo[64] = {};
   int dev = 0, n_sm = 0, occ = 0;
@@ -192,6 +209,11 @@ unsigned pages_grid(size_t n_pages) {
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_coalesced<R>, 256, 0);
         else if constexpr (Variant == 2)
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_async<R, 0>, 256, 0);
+        else if constexpr (Variant == 3) {
+          cudaError_t e2 = v6_opt_in<R, 0>();
+          if (e2 != cudaSuccess) return e2;
+          return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_warp<R, 0>, 256, pc::kV6Smem);
+        }
         else
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
       }) != cudaSuccess)
@@ -199,7 +221,7 @@ unsigned pages_grid(size_t n_pages) {
   // v5 at ChaCha12 runs best at 2 of its 4 resident CTAs per SM: 2835 vs
   // 2774 GB/s through bench.py (profiles/r01_ctas_ab.txt) -- fewer
   // concurrent page streams, same ALU feed (ILP 4 per thread)
-  const int dflt = (Variant == 2 && R == 12) ? std::min(occ, 2) : occ;
+  const int dflt = ((Variant == 2 || Variant == 3) && R == 12) ? std::min(occ, 2) : occ;
   const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : dflt;
   const uint64_t want = static_cast<uint64_t>(n_sm) * per_sm;
   const uint64_t slots = (n_pages + 3) / 4;
@@ -229,6 +251,25 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
         case 1: pc::k_crypt_pages_async<R, 1><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
         case 2: pc::k_crypt_pages_async<R, 2><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
         default: pc::k_crypt_pages_async<R, 3><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
+      }
+      counted();
+    }
+  }
+  else if (kern == 6) {
+    constexpr size_t kMax = size_t(1) << 30;
+    for (size_t p0 = 0; p0 < n_pages; p0 += kMax) {
+      const uint32_t m = static_cast<uint32_t>(std::min(kMax, n_pages - p0));
+      pc::PageDesc dd{d.vaddrs ? d.vaddrs + p0 : nullptr, d.pids ? d.pids + p0 : nullptr,
+                      d.vaddr0 + 4096ull * p0, d.pid0};
+      const unsigned grid = pages_grid<R, 3>(m);
+      const auto a = i4 + p0 * 256;
+      const auto b = o4 + p0 * 256;
+      constexpr size_t sm = pc::kV6Smem;
+      switch ((dd.vaddrs ? 1 : 0) | (dd.pids ? 2 : 0)) {
+        case 0: v6_opt_in<R, 0>(); pc::k_crypt_pages_warp<R, 0><<<grid, 256, sm, st>>>(key, dd, a, b, m); break;
+        case 1: v6_opt_in<R, 1>(); pc::k_crypt_pages_warp<R, 1><<<grid, 256, sm, st>>>(key, dd, a, b, m); break;
+        case 2: v6_opt_in<R, 2>(); pc::k_crypt_pages_warp<R, 2><<<grid, 256, sm, st>>>(key, dd, a, b, m); break;
+        default: v6_opt_in<R, 3>(); pc::k_crypt_pages_warp<R, 3><<<grid, 256, sm, st>>>(key, dd, a, b, m); break;
       }
       counted();
     }
@@ -323,7 +364,7 @@ int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, voi
       default: return launch_tma_r<20>(key, d, in, out, n_pages, st);
     }
   }
-  if (kern == 2 || kern == 3 || kern == 5) {
+  if (kern == 2 || kern == 3 || kern == 5 || kern == 6) {
     switch (rounds) {
       case 8: launch_pages_r<8>(kern, key, d, in, out, n_pages, st); break;
       case 12: launch_pages_r<12>(kern, key, d, in, out, n_pages, st); break;
@@ -1553,6 +1594,10 @@ cudaError_t touch_rounds() {
   acc(touch(pc::k_crypt_pages_async<R, 1>));
   acc(touch(pc::k_crypt_pages_async<R, 2>));
   acc(touch(pc::k_crypt_pages_async<R, 3>));
+  acc(v6_opt_in<R, 0>()); // loads the module and sets the shared-memory opt-in
+  acc(v6_opt_in<R, 1>());
+  acc(v6_opt_in<R, 2>());
+  acc(v6_opt_in<R, 3>());
   acc(touch(pc::k_keystream_seeds<R>));
   acc(touch(pc::k_service<R>));
   acc(touch(pc::k_slab_move<R, 0>));
@@ -2030,7 +2075,7 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "kernel")) {
-    if (value < 0 || value > 5) return fail(PC_EINVAL, "kernel must be 0 (auto) or 1..5");
+    if (value < 0 || value > 6) return fail(PC_EINVAL, "kernel must be 0 (auto) or 1..6");
     t.kernel = static_cast<int>(value);
     return PC_OK;
   }
