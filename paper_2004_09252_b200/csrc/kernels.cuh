@@ -639,7 +639,7 @@ __device__ __forceinline__ void slot_bar(uint32_t q) {
 }
 
 template <int ROUNDS, int DM>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, ROUNDS == 8 ? 3 : 4) // R=8 spills at 64 registers
 k_crypt_pages_warp(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out,
                    uint32_t n_pages) {
   constexpr bool VA = (DM & 1) != 0, PA = (DM & 2) != 0;

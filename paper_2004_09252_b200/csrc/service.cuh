@@ -73,6 +73,15 @@ __device__ __forceinline__ uint4 ld_volatile_v4(const uint4 *p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
   return r;
 }
+// LDG.128.STRONG.SYS + CCTL.IVALL: an acquire without the MEMBAR.SYS of a
+// fence (which waits for this SM's outstanding posted writes to host memory:
+// 1.9 us per request measured, profiles/r02_service_direct.txt)
+__device__ __forceinline__ uint4 ld_acquire_sys_v4(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.acquire.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
 __device__ __forceinline__ void st_volatile_v4(uint4 *p, uint4 v) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -120,8 +129,9 @@ template <int ROUNDS>
 __global__ void __launch_bounds__(64, 1)
 k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32_t ring, uint32_t n_workers,
           const SvcBell *host_bell, const uint32_t *host_stop, uint32_t *started, SvcDev *dev,
-          uint4 *hdr) {
+          uint4 *hdr, uint32_t direct) {
   __shared__ uint4 tile[256]; // one 4 KiB page
+  __shared__ uint4 bell_s;    // direct mode: the doorbell thread 0 saw (count, pid, vaddr)
   const uint32_t lane = threadIdx.x;
   if (blockIdx.x == n_workers) {
     if (threadIdx.x >= 32) return;
@@ -208,28 +218,57 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
   }
   SvcSlot *myring = slots + static_cast<uint64_t>(worker) * ring;
   uint4 *mypages = pages + static_cast<uint64_t>(worker) * ring * 256;
+  uint4 seen_bell = make_uint4(0, 0, 0, 0); // direct mode: last doorbell read (count, pid, vaddr)
   for (uint64_t head = 0;; ++head) {
-    // wait until ticket `head` is published (device-memory poll)
-    uint64_t bell;
-    for (;;) {
-      bell = ld_acquire_gpu(&dev->bell[worker]);
-      if (bell > head) break;
-      if (*reinterpret_cast<volatile uint32_t *>(&dev->stop)) return;
-      __nanosleep(32);
+    uint4 hd;
+    if (direct) {
+      // direct mode: the worker polls its own doorbell in host memory (one
+      // PCIe read per poll, no dispatcher hop); the newest ticket's header
+      // rides in the doorbell
+      if (seen_bell.x == static_cast<uint32_t>(head)) { // nothing published beyond head yet
+        if (tid == 0) {
+          uint4 b;
+          for (uint32_t polls = 1;; ++polls) {
+            // acquire: the page reads below are ordered after the doorbell
+            b = ld_acquire_sys_v4(reinterpret_cast<const uint4 *>(host_bell + worker));
+            if (b.x != static_cast<uint32_t>(head)) break;
+            if ((polls & 255) == 0 && ld_volatile_u32(host_stop) != 0u) {
+              b.x = static_cast<uint32_t>(head); // stop marker: count unchanged
+              b.y = 0xffffffffu; b.z = b.w = 0xffffffffu;
+              break;
+            }
+          }
+          bell_s = b;
+        }
+        named_bar(64);
+        seen_bell = bell_s;
+        named_bar(64); // bell_s may be rewritten by the next request
+        if (seen_bell.x == static_cast<uint32_t>(head)) return; // stop
+      }
+      const uint32_t newest = seen_bell.x - 1;
+      hd = make_uint4(seen_bell.z, seen_bell.w, seen_bell.y, newest);
+    } else {
+      // wait until ticket `head` is published (device-memory poll)
+      for (;;) {
+        const uint64_t bell = ld_acquire_gpu(&dev->bell[worker]);
+        if (bell > head) break;
+        if (*reinterpret_cast<volatile uint32_t *>(&dev->stop)) return;
+        __nanosleep(32);
+      }
     }
     uint64_t t0, t1, t2, t3;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     SvcSlot *sl = myring + (head % ring);
     uint4 *page = mypages + (head % ring) * 256;
-    // page loads go out first; when `head` is the latest forwarded ticket its
-    // header is already in device memory, so the keystream is computed while
-    // the page bytes cross PCIe; otherwise the header comes from the slot
+    // page loads go out first; when `head` is the latest published ticket its
+    // header came with the bell, so the keystream is computed while the page
+    // bytes cross PCIe; otherwise the header comes from the slot
     uint4 d[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) d[j] = ld_volatile_v4(page + 64 * j + tid);
     uint64_t vaddr;
     uint32_t pid;
-    const uint4 hd = ld_volatile_v4(&hdr[static_cast<uint64_t>(worker) * ring + head % ring]);
+    if (!direct) hd = ld_volatile_v4(&hdr[static_cast<uint64_t>(worker) * ring + head % ring]);
     if (hd.w == static_cast<uint32_t>(head)) { // header forwarded with the bell
       vaddr = static_cast<uint64_t>(hd.x) | (static_cast<uint64_t>(hd.y) << 32);
       pid = hd.z;

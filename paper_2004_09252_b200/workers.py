@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .engine import DeviceKey, _check_pid_int, _check_vaddr_int
+from .engine import DeviceKey, _check_pid_int, _check_vaddr_int, _fastmod
 from .errors import ContractViolation, PageCryptError, PoolError
 
 PAGE_SIZE = 4096
@@ -216,6 +216,16 @@ class WorkerPool:
         if direction not in ("encrypt", "decrypt"):
             raise ContractViolation(f"bad direction {direction!r}")
         data = getattr(page, "data", page)
+        fm = _fastmod()
+        if fm and 0 <= vaddr < 2**64 and not vaddr & 4095 and 0 <= client.pid < 2**32:
+            rc = fm.service_crypt_buf(self._svc, self.route(client), vaddr, client.pid, data, -1)
+            if rc == 0:
+                return
+            if rc > 0:
+                if rc == _native.PC_ETIMEOUT:
+                    raise PoolError("timed out waiting for crypto completion")
+                _native.check(rc)
+            # rc < 0: not a writable 4 KiB buffer -- the general path below reports it
         if type(data) is bytearray and len(data) == PAGE_SIZE:
             arr = _Page.from_buffer(data)  # cheapest way to its address (~1 us)
             ptr = arr
