@@ -830,10 +830,14 @@ def pager_rate(pc, key, device: int) -> dict:
 
     res = {}
     pages = [BASE_VADDR + PAGE * i for i in range(4096)]
-    for batch in (1, 64):
+    for batch, service in ((1, False), (1, True), (64, False)):
         st = DevicePageStore(8192, key, device=device)
+        if service:  # single faults as tickets of the store's resident worker
+            st.start_service()
         mem = {}
-        pg = WindowPager(st, lambda c, vs: np.stack([mem.pop(v) for v in vs]), window_capacity=64)
+        # the client hands back the page it holds (a single page as is)
+        pg = WindowPager(st, lambda c, vs: mem.pop(vs[0]) if len(vs) == 1 else np.stack([mem.pop(v) for v in vs]),
+                         window_capacity=64)
         c = ClientId(1, 0)
         pg.register(c)
         n = 0
@@ -850,7 +854,7 @@ def pager_rate(pc, key, device: int) -> dict:
                 n += len(vs)
         el = time.perf_counter() - t0
         m = pg.metrics[c]
-        res[f"batch{batch}"] = {"faults_per_s": round(n / el), "gbs": round(n * PAGE / el / 1e9, 3),
+        res[f"batch{batch}" + ("_service" if service else "")] = {"faults_per_s": round(n / el), "gbs": round(n * PAGE / el / 1e9, 3),
                                 "decrypts": m.decrypt_ops, "encrypts": m.encrypt_ops, "gpu_batches": m.gpu_batches}
         pg.unregister(c)
         st.close()

@@ -248,6 +248,16 @@ int pc_store_swap(pc_store *store, uint64_t client, uint32_t pid, const uint64_t
  * 0); evict_in (or NULL) is evicted to evict_vaddr; together one launch. */
 int pc_store_fault(pc_store *store, uint64_t client, uint32_t pid, uint64_t vaddr, void *out,
                    uint64_t evict_vaddr, const void *evict_in, int *refaulted);
+/* service: start (n_workers > 0) or stop (0) a resident worker service
+ * (section vii) started from the store's own key.  While it runs,
+ * pc_store_fault is one service ticket served by worker 0 (the slab read,
+ * both keystreams, the eviction's write into HBM and the refault's write to
+ * the host in one pass) instead of a launch + stream sync; batched calls keep
+ * their launches.  The store's requests are serialised by its lock, so one
+ * worker is enough.  pc_store_destroy stops it.  Replaces the launch in the
+ * worker thread's call of crypt_page on the fault path
+ * (pkg/src/pagecrypt/workers.py:130-142 <- orchestrator.py:197-198,234-235). */
+int pc_store_service(pc_store *store, int n_workers);
 
 /* ---- pinned host memory helpers ---------------------------------------
  * Note: freeing pinned memory (pc_host_free = cudaFreeHost) and

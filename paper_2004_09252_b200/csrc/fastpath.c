@@ -149,12 +149,62 @@ static PyObject *store_fault(PyObject *self, PyObject *const *args, Py_ssize_t n
   return Py_BuildValue("(ii)", rc, hit);
 }
 
+/* store_fault_buf(store, cid, pid, vaddr, out, evict_vaddr, evict) -> (rc, hit) or None
+ * pc_store_fault over buffer-protocol objects: out a writable C-contiguous
+ * 4096-byte buffer, evict None or a C-contiguous 4096-byte buffer.  None
+ * (no exception) when anything does not qualify -- a pid past u32, an
+ * unaligned vaddr, a wrong buffer -- so the caller's general path reports
+ * it with the reference's error. */
+static PyObject *store_fault_buf(PyObject *self, PyObject *const *args, Py_ssize_t nargs) {
+  (void)self;
+  uint64_t a[4], ev;
+  if (nargs != 7) {
+    PyErr_SetString(PyExc_TypeError, "store_fault_buf takes 7 arguments");
+    return NULL;
+  }
+  for (int i = 0; i < 4; ++i)
+    if (!as_u64(args[i], &a[i])) {
+      PyErr_Clear();
+      Py_RETURN_NONE;
+    }
+  if (!as_u64(args[5], &ev)) {
+    PyErr_Clear();
+    Py_RETURN_NONE;
+  }
+  if (a[2] > 0xffffffffull || (a[3] & 4095) || (ev & 4095)) Py_RETURN_NONE;
+  Py_buffer out, in;
+  if (PyObject_GetBuffer(args[4], &out, PyBUF_C_CONTIGUOUS | PyBUF_WRITABLE) != 0) {
+    PyErr_Clear();
+    Py_RETURN_NONE;
+  }
+  const int have_in = args[6] != Py_None;
+  if (have_in && PyObject_GetBuffer(args[6], &in, PyBUF_C_CONTIGUOUS) != 0) {
+    PyErr_Clear();
+    PyBuffer_Release(&out);
+    Py_RETURN_NONE;
+  }
+  if (out.len != PC_PAGE_SIZE || (have_in && in.len != PC_PAGE_SIZE)) {
+    if (have_in) PyBuffer_Release(&in);
+    PyBuffer_Release(&out);
+    Py_RETURN_NONE;
+  }
+  int hit = 0, rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = pc_store_fault((pc_store *)(uintptr_t)a[0], a[1], (uint32_t)a[2], a[3], out.buf, ev,
+                      have_in ? in.buf : NULL, &hit);
+  Py_END_ALLOW_THREADS
+  if (have_in) PyBuffer_Release(&in);
+  PyBuffer_Release(&out);
+  return Py_BuildValue("(ii)", rc, hit);
+}
+
 static PyMethodDef methods[] = {
     {"crypt_host", (PyCFunction)(void (*)(void))crypt_host, METH_FASTCALL, "pc_crypt_pages_host, contiguous"},
     {"crypt_host_buf", (PyCFunction)(void (*)(void))crypt_host_buf, METH_FASTCALL, "crypt_host over buffers"},
     {"service_crypt", (PyCFunction)(void (*)(void))service_crypt, METH_FASTCALL, "pc_service_crypt"},
     {"service_crypt_buf", (PyCFunction)(void (*)(void))service_crypt_buf, METH_FASTCALL, "service_crypt in place"},
     {"store_fault", (PyCFunction)(void (*)(void))store_fault, METH_FASTCALL, "pc_store_fault"},
+    {"store_fault_buf", (PyCFunction)(void (*)(void))store_fault_buf, METH_FASTCALL, "pc_store_fault on buffers"},
     {NULL, NULL, 0, NULL},
 };
 

@@ -597,6 +597,7 @@ struct pc_key {
   std::mutex mu;
   std::atomic<int> refs{0}; // stores holding this key; destroy refuses while > 0
   void *ipc_buf = nullptr;  // live CUDA-IPC export of the key (pc_key_export), or NULL
+  uint64_t serial = 0;      // process-unique identity (a service started from this key records it)
 };
 
 namespace {
@@ -626,8 +627,10 @@ void key_free(pc_key *k) {
 // private stream and event and a zeroed 256-byte stream-ordered slot.
 int key_new(int device, pc_key **out) {
   *out = nullptr;
+  static std::atomic<uint64_t> next_serial{1};
   auto *k = new pc_key();
   k->magic = kKeyMagic;
+  k->serial = next_serial.fetch_add(1);
   k->device = device;
   cudaError_t e = cudaStreamCreateWithFlags(&k->kst, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&k->ev, cudaEventDisableTiming);
@@ -1639,7 +1642,7 @@ constexpr uint32_t kServiceMagic = 0x73766331u; // "svc1"
 
 int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key, pc::SvcSlot *slots,
                    uint4 *pages, uint32_t ring, const pc::SvcBell *bell, const uint32_t *stop, uint32_t *started,
-                   pc::SvcDev *dev, uint4 *hdr) {
+                   pc::SvcDev *dev, uint4 *hdr, const pc::SvcOp *ops) {
   // direct: every worker polls its own doorbell; else one extra CTA is the dispatcher
   // auto (2): direct polling while few workers poll -- 8.6 vs 10.0 us per
   // 1-page request at 16 workers, but 148 pollers congest PCIe (11.2 us)
@@ -1648,9 +1651,9 @@ int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key
   const unsigned grid = static_cast<unsigned>(workers) + (direct ? 0 : 1);
   const uint32_t nw = static_cast<uint32_t>(workers);
   switch (rounds) {
-    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct); break;
-    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct); break;
-    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct); break;
+    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops); break;
+    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops); break;
+    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops); break;
   }
   counted();
   CU(cudaGetLastError());
@@ -1704,6 +1707,8 @@ struct pc_service {
   uint32_t *h_ctrl = nullptr, *d_ctrl = nullptr;      // [0] stop, [64..] started[w]
   pc::SvcBell *h_bell = nullptr, *d_bell = nullptr;   // per worker: tickets published (in order) + header
   pc::SvcDev *dev = nullptr;                          // device-memory doorbell mirror
+  pc::SvcOp *h_ops = nullptr, *d_ops = nullptr;       // mapped pinned: per slot, a store op's line
+  uint64_t key_serial = 0;                            // the key the workers hold (pc_key::serial)
   uint4 *hdr = nullptr;                               // forwarded headers, n_workers x ring
   // Host-side slot protocol.  Slot j of a worker carries tickets j, j+R, ...
   //   next[j]  = the ticket whose result is the next to be delivered in slot j
@@ -1774,6 +1779,7 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     pinned_put(s->h_pages, ns * PC_PAGE_SIZE);
     pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
     pinned_put(s->h_bell, s->n_workers * sizeof(pc::SvcBell));
+    pinned_put(s->h_ops, ns * sizeof(pc::SvcOp));
     if (s->st) cudaStreamDestroy(s->st);
     delete s;
     return code;
@@ -1797,6 +1803,9 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
   CUS(pinned_get(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(pc::SvcBell)));
   std::memset(s->h_bell, 0, n_workers * sizeof(pc::SvcBell));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_bell), s->h_bell, 0));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_ops), nslots * sizeof(pc::SvcOp)));
+  std::memset(s->h_ops, 0, nslots * sizeof(pc::SvcOp));
+  CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_ops), s->h_ops, 0));
   CUS(cudaMallocAsync(reinterpret_cast<void **>(&s->dev), sizeof(pc::SvcDev), s->st));
   CUS(cudaMemsetAsync(s->dev, 0, sizeof(pc::SvcDev), s->st));
   CUS(cudaMallocAsync(reinterpret_cast<void **>(&s->hdr), nslots * sizeof(uint4), s->st));
@@ -1805,7 +1814,7 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
 #undef CUS
   // the kernel reads the key once; it must be resident before we report success
   rc = service_launch(rounds, n_workers, s->st, key->d_words, s->d_slots, reinterpret_cast<uint4 *>(s->d_pages),
-                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev, s->hdr);
+                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev, s->hdr, s->d_ops);
   if (rc != PC_OK) return bail(rc);
   const auto t0 = std::chrono::steady_clock::now();
   volatile uint32_t *started = s->h_ctrl + 64;
@@ -1823,6 +1832,7 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
       std::this_thread::yield();
     }
   }
+  s->key_serial = key->serial;
   g_services_on[s->device].fetch_add(1);
   *out = s;
   return PC_OK;
@@ -1865,12 +1875,15 @@ int svc_check(pc_service *s, int worker) {
 
 extern "C" {
 
-int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
-                      uint64_t *ticket) {
-  int rc = svc_check(s, worker);
-  if (rc != PC_OK) return rc;
-  if (s->stopped) return fail(PC_ESTATE, "service is not running");
-  if (!src || !ticket) return fail(PC_EINVAL, "src/ticket is NULL");
+} // extern "C"
+
+namespace {
+// Publish one ticket: the page (src, or nothing when src is NULL: the ring
+// page was wiped when its last result was delivered), the header, the op
+// line of a store op (op != NULL; its flags ride in vaddr's low 12 bits),
+// then the doorbell, in ticket order.
+int svc_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
+               const pc::SvcOp *op, uint64_t *ticket) {
   const uint64_t t = s->tail[worker].fetch_add(1, std::memory_order_relaxed);
   const size_t slot = svc_slot(s, worker, t);
   // back-pressure (WorkerRing.push blocks while full): the slot's previous
@@ -1883,7 +1896,8 @@ int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, c
   }
   s->in_flight.fetch_add(1, std::memory_order_relaxed);
   pc::SvcSlot *sl = s->h_slots + slot;
-  std::memcpy(s->h_pages + slot * PC_PAGE_SIZE, src, PC_PAGE_SIZE);
+  if (src) std::memcpy(s->h_pages + slot * PC_PAGE_SIZE, src, PC_PAGE_SIZE);
+  if (op) s->h_ops[slot] = *op;
   s->dst[slot].store(dst, std::memory_order_relaxed);
   sl->vaddr = vaddr;
   sl->pid = pid;
@@ -1907,6 +1921,19 @@ int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, c
   _mm_store_si128(reinterpret_cast<__m128i *>(hb), v);
   *ticket = t;
   return PC_OK;
+}
+} // namespace
+
+extern "C" {
+
+int pc_service_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
+                      uint64_t *ticket) {
+  int rc = svc_check(s, worker);
+  if (rc != PC_OK) return rc;
+  if (s->stopped) return fail(PC_ESTATE, "service is not running");
+  if (!src || !ticket) return fail(PC_EINVAL, "src/ticket is NULL");
+  if (vaddr & 4095) return fail(PC_EINVAL, "vaddr %#llx not page-aligned", (unsigned long long)vaddr);
+  return svc_submit(s, worker, vaddr, pid, src, dst, nullptr, ticket);
 }
 
 int pc_service_poll(pc_service *s, int worker, uint64_t t, int *done) {
@@ -1981,6 +2008,7 @@ int pc_service_stop(pc_service *s) {
   pinned_put(s->h_pages, nslots * PC_PAGE_SIZE);
   pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
   pinned_put(s->h_bell, s->n_workers * sizeof(pc::SvcBell));
+  pinned_put(s->h_ops, nslots * sizeof(pc::SvcOp));
   cudaStreamDestroy(s->st);
   s->magic = 0;
   delete s;

@@ -95,6 +95,22 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t *p, uint32_t v) {
 // (conflict-free for both the coalesced and the per-lane 128-byte patterns).
 __device__ __forceinline__ uint32_t svc_swz(uint32_t q) { return (q & ~7u) | ((q ^ (q >> 3)) & 7u); }
 
+// A page-store operation riding a service ticket: the pager's single fault
+// (refault out of the HBM slab and the eviction its window admission forces,
+// /root/reference/pkg/src/pagecrypt/orchestrator.py:175-240) served by a
+// resident worker instead of a kernel launch (pc_store_service).  The
+// ticket's vaddr carries the op flags in its low 12 bits (vaddrs are page
+// aligned); the rest lives in the slot's SvcOp line (mapped host memory).
+struct alignas(64) SvcOp {
+  uint64_t slab;        // device address of the store's slab (4 KiB slots)
+  uint64_t evict_vaddr; // kOpPut: vaddr the ring page's plaintext is evicted to
+  uint32_t get_slot;    // kOpGet: slab slot decrypted into the ring page, then zeroed
+  uint32_t put_slot;    // kOpPut: slab slot the ring page is encrypted into
+  uint32_t pad[10];
+};
+static_assert(sizeof(SvcOp) == 64, "one 64-byte line per ring slot");
+constexpr uint32_t kOpStore = 1, kOpGet = 2, kOpPut = 4;
+
 // Device-side control block (device memory).
 // Host doorbell of one worker (mapped pinned memory, 16 bytes, written by
 // the producer that publishes ticket t: vaddr and pid of t first, then
@@ -129,7 +145,7 @@ template <int ROUNDS>
 __global__ void __launch_bounds__(64, 1)
 k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32_t ring, uint32_t n_workers,
           const SvcBell *host_bell, const uint32_t *host_stop, uint32_t *started, SvcDev *dev,
-          uint4 *hdr, uint32_t direct) {
+          uint4 *hdr, uint32_t direct, const SvcOp *ops) {
   __shared__ uint4 tile[256]; // one 4 KiB page
   __shared__ uint4 bell_s;    // direct mode: the doorbell thread 0 saw (count, pid, vaddr)
   const uint32_t lane = threadIdx.x;
@@ -276,7 +292,63 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
       vaddr = *reinterpret_cast<volatile uint64_t *>(&sl->vaddr);
       pid = *reinterpret_cast<volatile uint32_t *>(&sl->pid);
     }
+    const uint32_t op = static_cast<uint32_t>(vaddr) & 4095u;
+    vaddr &= ~uint64_t(4095);
     uint32_t x[16];
+    if (op & kOpStore) {
+      // ---- store op: refault (slab -> ring page) and/or evict (ring page -> slab)
+      const uint4 *oh = reinterpret_cast<const uint4 *>(ops + static_cast<uint64_t>(worker) * ring + head % ring);
+      const uint4 h0 = ld_volatile_v4(oh), h1 = ld_volatile_v4(oh + 1); // one PCIe read per warp
+      if (op & kOpGet) { // the refault keystream is computed while the op line crosses PCIe
+        const uint32_t sd[4] = {static_cast<uint32_t>(vaddr), static_cast<uint32_t>(vaddr >> 32), pid, tid};
+        chacha_block<ROUNDS, 0>(x, k, sd, rm);
+      }
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : : "memory");
+      uint4 *slab = reinterpret_cast<uint4 *>(static_cast<uint64_t>(h0.x) | (static_cast<uint64_t>(h0.y) << 32));
+      uint4 *gblk = slab + static_cast<uint64_t>(h1.x) * 256 + 4 * tid; // this thread's 64-byte block
+      uint4 *pblk = slab + static_cast<uint64_t>(h1.y) * 256 + 4 * tid;
+      uint4 c[4];
+      if (op & kOpGet) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = gblk[j];
+      }
+      if (op & kOpPut) {
+        uint32_t y[16];
+        const uint64_t ev = static_cast<uint64_t>(h0.z) | (static_cast<uint64_t>(h0.w) << 32);
+        const uint32_t se[4] = {static_cast<uint32_t>(ev), static_cast<uint32_t>(ev >> 32), pid, tid};
+        chacha_block<ROUNDS, 0>(y, k, se, rm);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tile[svc_swz(64 * j + tid)] = d[j];
+        named_bar(64);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 v = tile[svc_swz(4 * tid + q)];
+          v.x ^= y[4 * q]; v.y ^= y[4 * q + 1]; v.z ^= y[4 * q + 2]; v.w ^= y[4 * q + 3];
+          pblk[q] = v;
+        }
+        named_bar(64); // tile free again
+      }
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2) : : "memory");
+      if (op & kOpGet) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 v = c[q];
+          v.x ^= x[4 * q]; v.y ^= x[4 * q + 1]; v.z ^= x[4 * q + 2]; v.w ^= x[4 * q + 3];
+          tile[svc_swz(4 * tid + q)] = v;
+          if (!(op & kOpPut) || h1.x != h1.y) gblk[q] = make_uint4(0, 0, 0, 0); // refaulted slot wiped
+        }
+        named_bar(64);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) st_volatile_v4(page + 64 * j + tid, tile[svc_swz(64 * j + tid)]);
+      }
+      named_bar(64); // every thread's stores before thread 0's release
+      if (tid == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3) : : "memory");
+        sl->t_ns[0] = t0; sl->t_ns[1] = t1; sl->t_ns[2] = t2; sl->t_ns[3] = t3;
+        st_release_sys(&sl->done_seq, head + 1);
+      }
+      continue;
+    }
     const uint32_t sd[4] = {static_cast<uint32_t>(vaddr), static_cast<uint32_t>(vaddr >> 32), pid, tid};
     chacha_block<ROUNDS, 0>(x, k, sd, rm);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : : "memory");

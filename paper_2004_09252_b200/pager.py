@@ -117,15 +117,18 @@ class WindowPager:
         self.window_capacity = window_capacity
         self._windows: dict[object, SlidingWindow] = {}
         self.metrics: dict[object, PagerMetrics] = {}
+        self._state: dict[object, tuple] = {}  # client -> (window, metrics): one lookup per fault
 
     def register(self, client) -> None:
         if client in self._windows:
             raise ContractViolation(f"client {client} already registered")
         self._windows[client] = SlidingWindow(self.window_capacity)
         self.metrics[client] = PagerMetrics()
+        self._state[client] = (self._windows[client], self.metrics[client])
 
     def unregister(self, client) -> None:
         """Drop all server-side state of a client; its ciphertext is wiped."""
+        self._state.pop(client, None)
         if self._windows.pop(client, None) is not None:
             self.store.drop_client(client)
 
@@ -219,8 +222,10 @@ class WindowPager:
         """fault_batch for one page (the reference's flow): the same steps
         without the batch bookkeeping.  The page it evicts (if any) was
         resident before, so a refault and its eviction are one swap."""
-        win = self._window(client)
-        m = self.metrics[client]
+        st = self._state.get(client)
+        if st is None:
+            raise ContractViolation(f"unknown client {client}")
+        win, m = st
         v = int(vaddr)
         if v % PAGE_SIZE:
             raise ContractViolation(f"vaddr {v:#x} not page-aligned")
@@ -267,10 +272,24 @@ class WindowPager:
         e = win.admit(v)
         out = np.zeros((1, PAGE_SIZE), dtype=np.uint8)  # stays zero on a first touch
         try:
-            plain_ev = self._from_client(client, [e])[0] if e is not None else None
-            refault = native(client, v, out[0], e, plain_ev)
-            if plain_ev is not None:
-                plain_ev.fill(0)  # scratch_evict.wipe(), orchestrator.py:239
+            if e is None:
+                refault = native(client, v, out[0], None, None)
+            else:
+                # no private copy here: the library copies the page into its
+                # own staging (the server's scratch_evict) and wipes it there
+                # (orchestrator.py:230-239); the client's buffer is only read
+                got = self.fetch_evicted(client, [e])
+                plain_ev = got if type(got) is np.ndarray else np.asarray(got)
+                if plain_ev.dtype != np.uint8 or plain_ev.size != PAGE_SIZE or not plain_ev.flags.c_contiguous:
+                    plain_ev = np.array(plain_ev, dtype=np.uint8, copy=True, order="C")
+                    if plain_ev.size != PAGE_SIZE:
+                        raise ContractViolation(f"fetch_evicted returned {plain_ev.size} bytes for one page")
+                    try:
+                        refault = native(client, v, out[0], e, plain_ev.reshape(PAGE_SIZE))
+                    finally:
+                        plain_ev.fill(0)  # our private copy: scratch_evict.wipe()
+                else:
+                    refault = native(client, v, out[0], e, plain_ev.reshape(PAGE_SIZE))
         except BaseException:
             win.undo_admits([v], [e])
             raise

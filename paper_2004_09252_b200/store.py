@@ -33,7 +33,7 @@ import ctypes
 import numpy as np
 
 from . import _native
-from .engine import DeviceKey, Engine, _addr, _host_vaddrs, default_engine
+from .engine import DeviceKey, Engine, _addr, _fastmod, _host_vaddrs, default_engine
 from .errors import ContractViolation, PageCryptError
 
 PAGE_SIZE = 4096
@@ -71,12 +71,37 @@ class DevicePageStore:
 
     def _call(self, name, *args):
         rc = getattr(self._lib, name)(*args)
+        if rc:
+            self._raise(rc)
+
+    def _raise(self, rc: int):
         if rc == _native.PC_EFULL:
             raise StoreFull(self._lib.pc_last_error().decode())
         _native.check(rc)
 
+    def start_service(self, n_workers: int = 1) -> None:
+        """Serve single faults (``fault``) from a resident GPU worker started
+        with the store's key (``pc_store_service``): one service ticket per
+        fault instead of a kernel launch and a stream sync.  Batched calls
+        keep their launches.  ``close`` stops it."""
+        if n_workers < 1:
+            raise ContractViolation(f"n_workers must be >= 1, got {n_workers}")
+        self._need_key()
+        _native.call("pc_store_service", self._h, n_workers)
+        self._service = True
+
+    def stop_service(self) -> None:
+        if self._h is not None and getattr(self, "_service", False):
+            _native.call("pc_store_service", self._h, 0)
+        self._service = False
+
+    @property
+    def service_running(self) -> bool:
+        return getattr(self, "_service", False)
+
     def close(self) -> None:
         """Wipe the slab and free it."""
+        self._service = False  # pc_store_destroy stops it
         if self._h is not None:
             h, self._h = self._h, None
             _native.call("pc_store_destroy", h)
@@ -237,6 +262,17 @@ class DevicePageStore:
         self._need_key()
         if vaddr % PAGE_SIZE or not 0 <= vaddr < 2**64:
             raise ContractViolation(f"vaddr {vaddr:#x} not a page-aligned u64")
+        fm = _fastmod()
+        if fm and self._h is not None:
+            # METH_FASTCALL into pc_store_fault (csrc/fastpath.c): the buffer
+            # checks run in C; anything unusual comes back as None and takes
+            # the general path below, which reports it
+            r = fm.store_fault_buf(self._h, _cid(client), client.pid, vaddr, out,
+                                   0 if evict_plain is None else evict_vaddr, evict_plain)
+            if r is not None:
+                if r[0]:
+                    self._raise(r[0])
+                return bool(r[1])
         if out.nbytes != PAGE_SIZE or not out.flags.c_contiguous or not out.flags.writeable:
             raise ContractViolation("out must be a writable C-contiguous 4096-byte array")
         ev = None

@@ -53,6 +53,11 @@ class ClientId:
             raise ContractViolation(f"pid {self.pid} not a u32")
         if not 0 <= self.epoch < 2**32:
             raise ContractViolation(f"epoch {self.epoch} not a u32")
+        # the fault path looks clients up in dicts on every fault: hash once
+        object.__setattr__(self, "_hash", hash((self.pid, self.epoch)))
+
+    def __hash__(self):
+        return self._hash
 
 
 def _page_view(page) -> np.ndarray:

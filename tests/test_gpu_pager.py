@@ -62,11 +62,14 @@ def dkey(cuda):
     k.destroy()
 
 
+@pytest.mark.parametrize("service", [False, True], ids=["launch", "service"])
 @pytest.mark.parametrize("batch", [1, 3, 8, 20])
-def test_trace_matches_reference_semantics(dkey, batch):
+def test_trace_matches_reference_semantics(dkey, batch, service):
     W = 8
     rng = random.Random(batch)
     store = DevicePageStore(512, dkey)
+    if service:  # single faults through the resident worker, batches still launch
+        store.start_service()
     client_mem = {}
 
     def fetch(client, vaddrs):
@@ -98,9 +101,12 @@ def test_trace_matches_reference_semantics(dkey, batch):
     assert store.page_count(C) == 0
 
 
-def test_single_fault_matches_orchestrator_flow(dkey):
+@pytest.mark.parametrize("service", [False, True], ids=["launch", "service"])
+def test_single_fault_matches_orchestrator_flow(dkey, service):
     """W=1: every fault evicts the previous page (test_orchestrator.py:212-229 style)."""
     store = DevicePageStore(16, dkey)
+    if service:
+        store.start_service()
     mem = {}
     pager = WindowPager(store, lambda c, vs: np.stack([np.frombuffer(mem.pop(v), np.uint8) for v in vs]), 1)
     pager.register(C)

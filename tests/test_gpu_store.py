@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2004_09252_b200 as pc
-from paper_2004_09252_b200.errors import ContractViolation
+from paper_2004_09252_b200.errors import ContractViolation, PageCryptError
 from paper_2004_09252_b200.store import DevicePageStore, StoreFull
 from paper_2004_09252_b200.workers import ClientId
 
@@ -295,10 +295,14 @@ def test_stored_ciphertext_histogram(dkey):
     s.close()
 
 
-def test_native_fault_entry(dkey):
+@pytest.mark.parametrize("service", [False, True], ids=["launch", "service"])
+def test_native_fault_entry(dkey, service):
     """DevicePageStore.fault (pc_store_fault): one orchestrator fault --
-    lookup, refault and the forced eviction -- in one call."""
+    lookup, refault and the forced eviction -- in one call (one launch, or
+    one ticket of the store's resident worker)."""
     s = DevicePageStore(8, dkey)
+    if service:
+        s.start_service()
     out = np.full(4096, 7, np.uint8)
     assert s.fault(C1, 0x1000, out) is False and (out == 7).all()  # first touch: untouched
     assert s.fault(C1, 0x2000, out, 0x1000, np.frombuffer(page(1), np.uint8)) is False
@@ -332,3 +336,82 @@ def test_out_of_range_vaddrs_never_alias_stored_pages(dkey):
             s.insert(C1, bad, bytes(4096))
     assert s.refault(C1, top) == bytes(4096)
     s.close()
+
+
+@pytest.mark.parametrize("rounds", [8, 12, 20])
+def test_service_faults_match_launch_faults(dkey, rounds):
+    """A random fault stream (refault + eviction, refault only, eviction only,
+    first touch) through the resident worker gives the same outputs, the
+    same stored ciphertext (== the oracle's) and the same free-slot count as
+    the same stream through pc_store_swap launches."""
+    rng = np.random.default_rng(rounds)
+    stores = [DevicePageStore(40, dkey, rounds=rounds) for _ in range(2)]
+    stores[1].start_service()
+    assert stores[1].service_running and not stores[0].service_running
+    held = {}  # vaddr -> plaintext the client holds (evictable)
+    stored = set()
+    for step in range(300):
+        v = 0x7000_0000 + 4096 * int(rng.integers(0, 64))
+        if v in held:
+            continue
+        ev = None
+        if held and (rng.random() < 0.7 or len(stored) >= 38):
+            ev = list(held)[int(rng.integers(0, len(held)))]
+        if ev is None and len(stored) >= 38:
+            continue
+        outs = []
+        for s in stores:
+            out = np.full(4096, 0xEE, np.uint8)
+            plain = None if ev is None else np.frombuffer(held[ev], np.uint8).copy()
+            hit = s.fault(C1, v, out, ev, plain)
+            outs.append((hit, out.tobytes()))
+        assert outs[0] == outs[1], step
+        hit, got = outs[0]
+        assert hit == (v in stored)
+        if ev is not None:
+            stored.add(ev)
+            del held[ev]
+        if hit:
+            stored.discard(v)
+        held[v] = (got if hit else bytes(4096))[:7] + rng.bytes(4096 - 7)
+    for s in stores:
+        assert s.free_slots == 40 - len(stored)
+        for v in stored:
+            assert s.lookup(C1, v) == stores[0].lookup(C1, v)
+    for v in list(stored)[:5]:
+        plain = stores[1].refault(C1, v)
+        want = C.crypt_pages(KEY, np.array([v], np.uint64), np.array([C1.pid], np.uint32),
+                             np.frombuffer(plain, np.uint8).reshape(1, 4096), rounds=rounds)
+        assert stores[0].lookup(C1, v) == want.tobytes()
+    stores[1].stop_service()
+    assert not stores[1].service_running
+    for s in stores:
+        s.close()
+
+
+def test_service_fault_errors_leave_store_unchanged(dkey):
+    """Errors on the service path are the launch path's: a duplicate insert,
+    a full store, bad arguments -- and nothing changes."""
+    s = DevicePageStore(1, dkey)
+    s.start_service()
+    out = np.zeros(4096, np.uint8)
+    assert s.fault(C1, 0x2000, out, 0x1000, np.frombuffer(page(1), np.uint8)) is False
+    with pytest.raises(StoreFull):  # first touch + eviction into a full slab
+        s.fault(C1, 0x3000, out, 0x4000, np.frombuffer(page(2), np.uint8))
+    with pytest.raises(ContractViolation):  # 0x1000 is stored and not refaulted by this fault
+        s.fault(C1, 0x5000, out, 0x1000, np.frombuffer(page(3), np.uint8))
+    with pytest.raises(ContractViolation):
+        s.fault(C1, 0x1001, out)
+    assert s.free_slots == 0 and s.lookup(C1, 0x1000) == pc.crypt_page(KEY, 0x1000, C1.pid, page(1))
+    # refault + evict the same vaddr back in (the freed slot is reused)
+    assert s.fault(C1, 0x1000, out, 0x1000, np.frombuffer(page(4), np.uint8)) is True
+    assert out.tobytes() == page(1) and s.refault(C1, 0x1000) == page(4)
+    with pytest.raises(ContractViolation):
+        s.start_service(0)
+    with pytest.raises(PageCryptError):
+        s.start_service()  # already running
+    s.close()  # stops the worker
+    keyless = DevicePageStore(2)
+    with pytest.raises(PageCryptError):
+        keyless.start_service()
+    keyless.close()

@@ -105,14 +105,17 @@ def test_pager_reproduces_reference_orchestrator_on_cpu(traces, i):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("service", [False, True], ids=["launch", "service"])
 @pytest.mark.parametrize("i", [0, 1, 2])
-def test_pager_over_hbm_store_reproduces_reference_orchestrator(traces, i, cuda):
+def test_pager_over_hbm_store_reproduces_reference_orchestrator(traces, i, cuda, service):
     import paper_2004_09252_b200 as pc
     from paper_2004_09252_b200.store import DevicePageStore
 
     key = pc.DeviceKey.install(traces["key"].tobytes(), 0)
     try:
         store = DevicePageStore(64, key)
+        if service:  # every single fault through the store's resident worker
+            store.start_service()
         pager, client, reads = replay(traces, i, store)
         check(traces, i, pager, client, reads, list(store.pages(client)))
         store.close()
