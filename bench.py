@@ -790,6 +790,29 @@ def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
         p50 = ts[len(ts) // 2] / 1e3
         res[str(n)] = {"p50_us": round(p50, 2), "p99_us": round(ts[int(len(ts) * 0.99)] / 1e3, 2),
                        "gbps_at_p50": round(n * PAGE / (p50 * 1e-6) / 1e9, 3)}
+    # the same calls with resident workers on the key (DeviceKey.start_service):
+    # 1-2 page batches become service tickets instead of launches
+    dk = pc.DeviceKey.generate(device)
+    try:
+        dk.start_service(n_workers=2)
+        res["resident_workers"] = {}
+        for n in (1, 2, 4):
+            src = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8).pin_memory()
+            dst = torch.empty_like(src).pin_memory()
+            for _ in range(300):
+                pc.crypt_pages(dk, BASE_VADDR, 1, src, out=dst)
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter_ns()
+                pc.crypt_pages(dk, BASE_VADDR, 1, src, out=dst)
+                ts.append(time.perf_counter_ns() - t0)
+            ts.sort()
+            p50 = ts[len(ts) // 2] / 1e3
+            res["resident_workers"][str(n)] = {"p50_us": round(p50, 2),
+                                               "p99_us": round(ts[int(len(ts) * 0.99)] / 1e3, 2)}
+        res["resident_workers"]["workers"] = 2
+    finally:
+        dk.destroy()
     return res
 
 

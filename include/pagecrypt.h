@@ -191,8 +191,17 @@ int pc_service_in_flight(pc_service *svc, uint64_t *n);
 /* Diagnostics: device %globaltimer stamps of the slot's last request (bell
  * seen, page loaded, keystream done, page written back). */
 int pc_service_timing(pc_service *svc, int worker, uint64_t ticket, uint64_t out_ns[4]);
+/* diagnostic: the SM (%smid) worker `worker` runs on */
+int pc_service_worker_sm(pc_service *svc, int worker, int *smid);
 int pc_service_max_workers(int device, int *n);
 int pc_service_stop(pc_service *svc);
+/* key service: start (n_workers > 0) or stop (0) resident workers holding
+ * `key` (this section's kernel).  While they run, pc_crypt_pages_host calls
+ * under `key` with `rounds` on at most svc_pages host pages (pc_tune knob;
+ * 0 = 2 per worker) are one service ticket per page instead of a launch --
+ * the fault handler's 1-2 page calls (orchestrator.py:197-198,234-235) skip
+ * the launch and stream sync.  pc_key_destroy stops them. */
+int pc_key_service(pc_key *key, int n_workers, int rounds);
 
 /* ---- (viii) HBM page store (device-resident ciphertext) -----
  * The B200 side of EncryptedPageStore (pkg/src/pagecrypt/store.py:41-105)

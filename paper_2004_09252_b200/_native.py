@@ -81,6 +81,8 @@ SIGNATURES = {
     "pc_store_contains_many": (c_int, [c_void_p, c_u64, c_void_p, c_size_t, c_void_p]),
     "pc_store_fault": (c_int, [c_void_p, c_u64, c_u32, c_u64, c_void_p, c_u64, c_void_p, P(c_int)]),
     "pc_store_service": (c_int, [c_void_p, c_int]),
+    "pc_key_service": (c_int, [c_void_p, c_int, c_int]),
+    "pc_service_worker_sm": (c_int, [c_void_p, c_int, P(c_int)]),
     "pc_host_alloc": (c_int, [c_size_t, P(c_void_p)]),
     "pc_host_free": (c_int, [c_void_p]),
     "pc_host_register": (c_int, [c_void_p, c_size_t]),

@@ -86,6 +86,8 @@ struct Tuning {
   std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
   std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
+  std::atomic<int64_t> svc_pages{0};   // host batches up to this many pages go to the key's resident
+                                       // workers when it has them (pc_key_service); 0 = 2 per worker
   std::atomic<int> kernel{0};          // HBM kernel: 0 = auto (per rounds, below), 1 = k_crypt_blocks,
                                        // 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced,
                                        // 4 = k_crypt_pages_tma, 5 = k_crypt_pages_async,
@@ -598,6 +600,9 @@ struct pc_key {
   std::atomic<int> refs{0}; // stores holding this key; destroy refuses while > 0
   void *ipc_buf = nullptr;  // live CUDA-IPC export of the key (pc_key_export), or NULL
   uint64_t serial = 0;      // process-unique identity (a service started from this key records it)
+  pc_service *svc = nullptr; // resident workers for fault-sized host batches (pc_key_service)
+  int svc_rounds = 0;
+  int svc_workers = 0;
 };
 
 namespace {
@@ -804,6 +809,10 @@ int pc_key_destroy(pc_key *key) {
   if (key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
   if (const int r = key->refs.load())
     return fail(PC_ESTATE, "key is still held by %d page store(s); destroy them first", r);
+  if (key->svc) {
+    int rc = pc_key_service(key, 0, 0);
+    if (rc != PC_OK) return rc;
+  }
   DeviceGuard g(key->device);
   CU(g.err);
   if (key->ipc_buf) {
@@ -1263,6 +1272,32 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
 
 } // namespace
 
+namespace {
+int svc_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
+               const pc::SvcOp *op, uint64_t *ticket);
+int crypt_on_service(const pc_key *key, const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
+                     uint32_t pid0, const void *in, void *out, size_t n) {
+  uint64_t tickets[64];
+  const int W = key->svc_workers;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t va = vaddrs ? vaddrs[i] : vaddr0 + 4096ull * i;
+    const uint32_t pid = pids ? pids[i] : pid0;
+    int rc = svc_submit(key->svc, static_cast<int>(i % W), va, pid, static_cast<const uint8_t *>(in) + i * PC_PAGE_SIZE,
+                        static_cast<uint8_t *>(out) + i * PC_PAGE_SIZE, nullptr, &tickets[i]);
+    if (rc != PC_OK) {
+      for (size_t j = 0; j < i; ++j) pc_service_wait(key->svc, static_cast<int>(j % W), tickets[j], -1);
+      return rc;
+    }
+  }
+  int rc = PC_OK;
+  for (size_t i = 0; i < n; ++i) {
+    const int r = pc_service_wait(key->svc, static_cast<int>(i % W), tickets[i], -1);
+    if (rc == PC_OK) rc = r;
+  }
+  return rc;
+}
+} // namespace
+
 int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key, const uint64_t *vaddrs,
                         const uint32_t *pids, uint64_t vaddr0, uint32_t pid0, const void *in, void *out,
                         size_t n, int rounds) {
@@ -1279,6 +1314,15 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
   if (vaddrs)
     for (size_t i = 0; i < n; ++i)
       if (vaddrs[i] & 4095) return fail(PC_EINVAL, "vaddr %#llx not page-aligned", (unsigned long long)vaddrs[i]);
+  if (!raw_key && key->svc && key->svc_rounds == rounds) {
+    // fault-sized host batches on the key's resident workers: one ticket
+    // per page, spread over the workers, no launch
+    const int64_t lim = tuning().svc_pages.load();
+    const size_t max_pages = lim > 0 ? static_cast<size_t>(lim) : 2 * static_cast<size_t>(key->svc_workers);
+    int gin = -1, gout = -1;
+    if (n <= max_pages && !device_memory(in, &gin) && !device_memory(out, &gout))
+      return crypt_on_service(key, vaddrs, pids, vaddr0, pid0, in, out, n);
+  }
   std::lock_guard<std::mutex> lk(e->mu);
   DeviceGuard g(e->device);
   CU(g.err);
@@ -1778,7 +1822,7 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     pinned_put(s->h_slots, ns * sizeof(pc::SvcSlot));
     pinned_put(s->h_pages, ns * PC_PAGE_SIZE);
     pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
-    pinned_put(s->h_bell, s->n_workers * sizeof(pc::SvcBell));
+    pinned_put(s->h_bell, s->n_workers * pc::kBellStride * sizeof(pc::SvcBell));
     pinned_put(s->h_ops, ns * sizeof(pc::SvcOp));
     if (s->st) cudaStreamDestroy(s->st);
     delete s;
@@ -1800,8 +1844,8 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_slots), s->h_slots, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_pages), s->h_pages, 0));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_ctrl), s->h_ctrl, 0));
-  CUS(pinned_get(reinterpret_cast<void **>(&s->h_bell), n_workers * sizeof(pc::SvcBell)));
-  std::memset(s->h_bell, 0, n_workers * sizeof(pc::SvcBell));
+  CUS(pinned_get(reinterpret_cast<void **>(&s->h_bell), n_workers * pc::kBellStride * sizeof(pc::SvcBell)));
+  std::memset(s->h_bell, 0, n_workers * pc::kBellStride * sizeof(pc::SvcBell));
   CUS(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->d_bell), s->h_bell, 0));
   CUS(pinned_get(reinterpret_cast<void **>(&s->h_ops), nslots * sizeof(pc::SvcOp)));
   std::memset(s->h_ops, 0, nslots * sizeof(pc::SvcOp));
@@ -1904,7 +1948,7 @@ int svc_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const vo
   std::atomic_thread_fence(std::memory_order_release);
   // publish in ticket order: the doorbell counts consecutive published
   // tickets; the header of the newest one rides along (dispatcher fast path)
-  pc::SvcBell *hb = s->h_bell + worker;
+  pc::SvcBell *hb = s->h_bell + static_cast<size_t>(worker) * pc::kBellStride;
   auto *count = reinterpret_cast<std::atomic<uint32_t> *>(&hb->count);
   uint32_t bspins = 0;
   while (count->load(std::memory_order_acquire) != static_cast<uint32_t>(t)) {
@@ -1982,10 +2026,46 @@ int pc_service_timing(pc_service *s, int worker, uint64_t t, uint64_t out_ns[4])
   return PC_OK;
 }
 
+// Diagnostic: the SM a worker runs on (recorded when it started).
+int pc_service_worker_sm(pc_service *s, int worker, int *smid) {
+  int rc = svc_check(s, worker);
+  if (rc != PC_OK) return rc;
+  if (!smid) return fail(PC_EINVAL, "smid is NULL");
+  *smid = static_cast<int>(reinterpret_cast<volatile uint32_t *>(s->h_ctrl + 64)[worker]) - 1;
+  return PC_OK;
+}
+
 int pc_service_in_flight(pc_service *s, uint64_t *n) {
   if (!s || s->magic != kServiceMagic) return fail(PC_ESTATE, "not a live pc_service");
   if (!n) return fail(PC_EINVAL, "n is NULL");
   *n = s->in_flight.load();
+  return PC_OK;
+}
+
+// Resident workers for one key (section vii kernel, started from this key):
+// while they run, pc_crypt_pages_host batches of up to svc_pages host pages
+// under this key and round count are service tickets instead of launches.
+int pc_key_service(pc_key *key, int n_workers, int rounds) {
+  if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
+  if (n_workers < 0) return fail(PC_EINVAL, "n_workers must be >= 0, got %d", n_workers);
+  std::lock_guard<std::mutex> lk(key->mu);
+  if (n_workers == 0) {
+    if (!key->svc) return PC_OK;
+    int rc = pc_service_stop(key->svc);
+    if (rc != PC_OK) return rc;
+    key->svc = nullptr;
+    key->svc_workers = 0;
+    key->svc_rounds = 0;
+    return PC_OK;
+  }
+  if (key->svc) return fail(PC_ESTATE, "key already has resident workers");
+  if (!valid_rounds(rounds)) return fail(PC_EINVAL, "rounds must be 8, 12 or 20, got %d", rounds);
+  pc_service *s = nullptr;
+  int rc = pc_service_start(key, n_workers, 64, rounds, &s);
+  if (rc != PC_OK) return rc;
+  key->svc_rounds = rounds;
+  key->svc_workers = n_workers;
+  key->svc = s;
   return PC_OK;
 }
 
@@ -2007,7 +2087,7 @@ int pc_service_stop(pc_service *s) {
   pinned_put(s->h_slots, nslots * sizeof(pc::SvcSlot));
   pinned_put(s->h_pages, nslots * PC_PAGE_SIZE);
   pinned_put(s->h_ctrl, (64 + static_cast<size_t>(s->n_workers)) * 4);
-  pinned_put(s->h_bell, s->n_workers * sizeof(pc::SvcBell));
+  pinned_put(s->h_bell, s->n_workers * pc::kBellStride * sizeof(pc::SvcBell));
   pinned_put(s->h_ops, nslots * sizeof(pc::SvcOp));
   cudaStreamDestroy(s->st);
   s->magic = 0;
@@ -2108,6 +2188,11 @@ int pc_tune(const char *knob, int64_t value) {
       }
     return fail(PC_EINVAL, "rotmask %#llx is not a compiled variant", (unsigned long long)value);
   }
+  if (!std::strcmp(knob, "svc_pages")) {
+    if (value < 0 || value > 64) return fail(PC_EINVAL, "svc_pages must be 0..64");
+    t.svc_pages = value;
+    return PC_OK;
+  }
   if (!std::strcmp(knob, "small_mode")) {
     if (value != 0 && value != 1) return fail(PC_EINVAL, "small_mode must be 0 or 1");
     t.small_mode = static_cast<int>(value);
@@ -2151,6 +2236,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   Tuning &t = tuning();
   if (!std::strcmp(knob, "rotmask")) *value = t.rot_mask;
   else if (!std::strcmp(knob, "small_mode")) *value = t.small_mode;
+  else if (!std::strcmp(knob, "svc_pages")) *value = t.svc_pages.load();
   else if (!std::strcmp(knob, "small_max")) *value = static_cast<int64_t>(t.small_max.load());
   else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
   else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;

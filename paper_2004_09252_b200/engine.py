@@ -172,6 +172,22 @@ class DeviceKey:
             raise PageCryptError("device key already destroyed")
         return self._handle
 
+    def start_service(self, n_workers: int = 1, rounds: int = 20) -> None:
+        """Start resident GPU workers holding this key (``pc_key_service``):
+        host batches of up to 2 pages per worker under this key and round
+        count then run as service tickets instead of launches -- the fault
+        handler's 1-2 page calls skip the launch and the stream sync.
+        ``stop_service``/``destroy`` stop them."""
+        if n_workers < 1:
+            raise ContractViolation(f"n_workers must be >= 1, got {n_workers}")
+        if rounds not in (8, 12, 20):
+            raise ContractViolation(f"rounds must be 8, 12 or 20, got {rounds}")
+        _native.call("pc_key_service", self.handle, n_workers, rounds)
+
+    def stop_service(self) -> None:
+        if self._handle is not None:
+            _native.call("pc_key_service", self._handle, 0, 0)
+
     def destroy(self) -> None:
         """Zero the device copy and free it (workers.py:252-254).  Idempotent."""
         if self._handle is not None:

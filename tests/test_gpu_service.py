@@ -469,3 +469,50 @@ def test_device_checks_never_launch_foreign_kernels_beside_the_service(cuda, tmp
     r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=180, env=env,
                        cwd=root)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.returncode, r.stdout[-500:], r.stderr[-1500:])
+
+
+@pytest.mark.parametrize("rounds", [8, 12, 20])
+def test_key_service_small_host_batches_match_oracle(cuda, rounds):
+    """DeviceKey.start_service: fault-sized host batches (contiguous, per-page
+    vaddr/pid arrays, in place) run as service tickets and equal the oracle;
+    larger batches and other round counts keep the launch path; the knob
+    svc_pages moves the boundary; destroy() stops the workers."""
+    import paper_2004_09252_b200 as pc
+
+    key = bytes(range(40, 72))
+    rng = np.random.default_rng(rounds)
+    dk = pc.DeviceKey.install(key, 0)
+    dk.start_service(n_workers=2, rounds=rounds)
+    with pytest.raises(Exception):
+        dk.start_service()  # already running
+    before = _native.tune_get("launches")
+    for n in (1, 2, 3, 4):
+        pages = rng.integers(0, 256, (n, 4096), dtype=np.uint8)
+        va = (0x7F00_0000_0000 + 4096 * rng.permutation(64)[:n]).astype(np.uint64)
+        pids = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+        want = C.crypt_pages(key, va, pids, pages, rounds=rounds)
+        assert np.array_equal(pc.crypt_pages(dk, va, pids, pages, rounds=rounds), want)
+        want1 = C.crypt_pages(key, va[0] + 4096 * np.arange(n, dtype=np.uint64),
+                              np.full(n, 9, np.uint32), pages, rounds=rounds)
+        buf = pages.copy()
+        pc.crypt_pages(dk, int(va[0]), 9, buf, out=buf, rounds=rounds)  # in place, contiguous
+        assert np.array_equal(buf, want1)
+    assert _native.tune_get("launches") == before  # every batch above was <= 4 pages on 2 workers
+    pages = rng.integers(0, 256, (5, 4096), dtype=np.uint8)
+    want = C.crypt_pages(key, 0x1000 + 4096 * np.arange(5, dtype=np.uint64), np.full(5, 3, np.uint32), pages,
+                         rounds=rounds)
+    assert np.array_equal(pc.crypt_pages(dk, 0x1000, 3, pages, rounds=rounds), want)
+    assert _native.tune_get("launches") > before  # 5 pages > 2 per worker: the launch path
+    other = 20 if rounds != 20 else 8
+    before = _native.tune_get("launches")
+    pc.crypt_pages(dk, 0x1000, 3, pages[:1], rounds=other)
+    assert _native.tune_get("launches") > before  # the workers hold `rounds` only
+    _native.tune("svc_pages", 5)
+    try:
+        before = _native.tune_get("launches")
+        assert np.array_equal(pc.crypt_pages(dk, 0x1000, 3, pages, rounds=rounds), want)
+        assert _native.tune_get("launches") == before
+    finally:
+        _native.tune("svc_pages", 0)
+    dk.destroy()  # stops the workers first
+    assert dk.destroyed
