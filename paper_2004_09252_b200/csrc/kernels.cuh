@@ -554,7 +554,7 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
         if constexpr (VA) rv = __ldg(desc.vaddrs + page + 2 * stride);
         if constexpr (PA) rp = __ldg(desc.pids + page + 2 * stride);
       }
-      issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
+    issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
     if (!cached || s[1] != cached_hi) {
       c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
       quarter_round<0>(c1a, c1b, c1c, c1d, rm);
@@ -758,6 +758,131 @@ k_crypt_pages_warp(const uint32_t *__restrict__ key, PageDesc desc, const uint4 
     if (page >= n_pages) break;
     dst += step;
     st = st == 2 ? 0 : st + 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// v9: v5's cp.async page ring fed by a per-page seed table.  A pre-pass
+// (k_page_seed_table, one thread per page) computes the three page-only
+// quarter rounds of round 1 -- columns 0, 1, 2 start from (sigma_c, k_c,
+// k_c+4, word 12+c), i.e. vaddr_lo, vaddr_hi and the pid -- and files them
+// with state words 12..14 as one 64-byte record per page.  The page loop
+// streams each page's record into its ring stage next to the page bytes
+// (lanes 0-3 of each warp, one 16-byte cp.async each) and reads it back with
+// four broadcast LDS.128, so it runs no seed round and loads no descriptor:
+// only column 3 (the block index) is per thread, and it is hoisted.  Every
+// descriptor shape (contiguous, vaddr array, pid array) is the same loop.
+// Every block is still exactly ChaCha_R(state) + state.
+constexpr int kV9Stages = 4;
+constexpr size_t kV9Smem = kV9Stages * (256 * 4 * 16 + 8 * 64); // ring + one record per warp per stage
+
+__global__ void __launch_bounds__(256)
+k_page_seed_table(const uint32_t *__restrict__ key, PageDesc desc, uint4 *__restrict__ rec, uint32_t n_pages) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pages) return;
+  constexpr RotMul rm{};
+  uint32_t k[8];
+  load_key(key, k);
+  uint64_t va;
+  uint32_t pid;
+  desc_fetch(desc, p, va, pid);
+  const uint32_t lo = static_cast<uint32_t>(va), hi = static_cast<uint32_t>(va >> 32);
+  uint32_t a0 = kSigma0, b0 = k[0], c0 = k[4], d0 = lo;
+  uint32_t a1 = kSigma1, b1 = k[1], c1 = k[5], d1 = hi;
+  uint32_t a2 = kSigma2, b2 = k[2], c2 = k[6], d2 = pid;
+  quarter_round<0>(a0, b0, c0, d0, rm);
+  quarter_round<0>(a1, b1, c1, d1, rm);
+  quarter_round<0>(a2, b2, c2, d2, rm);
+  uint4 *r = rec + static_cast<uint64_t>(p) * 4;
+  r[0] = make_uint4(a0, b0, c0, d0);
+  r[1] = make_uint4(a1, b1, c1, d1);
+  r[2] = make_uint4(a2, b2, c2, d2);
+  r[3] = make_uint4(lo, hi, pid, 0);
+}
+
+// The record of page i+1 is read from shared memory at the end of page i
+// (after the wait that page i's bytes need anyway), so the next page's rounds
+// start from registers: no shared-memory latency at the top of the loop.
+template <int ROUNDS>
+__global__ void __launch_bounds__(256, 3)
+k_crypt_pages_seeded(const uint32_t *__restrict__ key, const uint4 *__restrict__ rec, const uint4 *in, uint4 *out,
+                     uint32_t n_pages) {
+  constexpr RotMul rm{};
+  constexpr int S = kV9Stages;
+  extern __shared__ __align__(128) uint4 v9_smem[];
+  uint4 *ring = v9_smem;                    // [stage][256 threads x 4 chunks]
+  uint4 *recs = v9_smem + S * 256 * 4;      // [stage][8 warps x 4 chunks]
+  const uint32_t tid = threadIdx.x;
+  const uint32_t b = tid & 63, lane = tid & 31, warp = tid >> 5;
+  const uint32_t sw = (tid >> 1) & 3;
+  const uint32_t stride = gridDim.x * 4;
+  uint32_t page = blockIdx.x * 4 + (tid >> 6);
+  if (page >= n_pages) return;
+  constexpr uint32_t kStageBytes = 256 * 4 * 16, kRecStage = 8 * 64;
+  const uint32_t base0 = smem_u32(ring + tid * 4);
+  const uint32_t rbase0 = smem_u32(recs + warp * 4 + (lane & 3));
+  const uint64_t step = static_cast<uint64_t>(stride) * 256;
+  const uint4 *src_ahead = in + static_cast<uint64_t>(page) * 256 + b * 4;
+  const uint4 *rec_ahead = rec + static_cast<uint64_t>(page) * 4 + (lane & 3);
+  uint4 *dst = out + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint32_t page_ahead = page;
+  auto issue = [&](int st) { // next page (bytes + record) for the ring, then advance
+    if (page_ahead < n_pages) {
+      const uint32_t sdst = base0 + st * kStageBytes;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async16(sdst + 16 * (c ^ sw), src_ahead + c);
+      if (lane < 4) cp_async16(rbase0 + st * kRecStage, rec_ahead);
+    }
+    cp_async_commit();
+    page_ahead += stride;
+    src_ahead += step;
+    rec_ahead += static_cast<uint64_t>(stride) * 4;
+  };
+#pragma unroll
+  for (int i = 0; i < S - 1; ++i) issue(i);
+  uint32_t k[8];
+  load_key(key, k);
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  cp_async_wait<S - 2>(); // page 0's group
+  __syncwarp();
+  uint4 r0 = recs[warp * 4], r1 = recs[warp * 4 + 1], r2 = recs[warp * 4 + 2], r3 = recs[warp * 4 + 3];
+  int st = 0;
+  for (;;) {
+    __syncwarp(); // every lane is past its reads of the stage the next issue overwrites
+    issue(st == 0 ? S - 1 : st - 1); // stage (st + S - 1) % S
+    uint32_t x[16];
+    x[0] = r0.x; x[4] = r0.y; x[8] = r0.z; x[12] = r0.w;
+    x[1] = r1.x; x[5] = r1.y; x[9] = r1.z; x[13] = r1.w;
+    x[2] = r2.x; x[6] = r2.y; x[10] = r2.z; x[14] = r2.w;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    const uint32_t s0 = r3.x, s1 = r3.y, s2 = r3.z;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int i = 1; i < ROUNDS / 2; ++i) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    cp_async_wait<S - 2>(); // the next page's group has landed (and this page's)
+    __syncwarp();           // lanes 0-3's record copies are visible to the warp
+    const int nst = st == S - 1 ? 0 : st + 1;
+    const uint4 *rn = recs + nst * 32 + warp * 4;
+    r0 = rn[0]; r1 = rn[1]; r2 = rn[2]; r3 = rn[3];
+    const uint4 *mine = ring + st * 1024 + tid * 4;
+    const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s0), d3.y ^ (x[13] + s1), d3.z ^ (x[14] + s2),
+                              d3.w ^ (x[15] + b)));
+    page += stride;
+    if (page >= n_pages) break;
+    dst += step;
+    st = nst;
   }
   cp_async_wait<0>();
 }

@@ -203,7 +203,42 @@ cudaError_t v6_opt_in() {
   return e;
 }
 
-template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async, 3 = v6 warp-shared seeds
+template <int R>
+cudaError_t v9_opt_in() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(pc::k_crypt_pages_seeded<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(pc::kV9Smem));
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// Stream-ordered scratch for v9's per-page seed records (64 B per page): a
+// private memory pool per device that keeps its memory (release threshold
+// max), so a launch's allocation is a pool hit, not a cudaMalloc.
+cudaMemPool_t seed_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t p = nullptr;
+  if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+  uint64_t keep = UINT64_MAX;
+  cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+  pools[dev] = p;
+  return p;
+}
+
+template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async, 3 = v6 warp-shared seeds, 4 = v9 seeded
 unsigned pages_grid(size_t n_pages) {
   static std::atomic<uint32_t> geo[64] = {};
   int dev = 0, n_sm = 0, occ = 0;
@@ -220,6 +255,11 @@ unsigned pages_grid(size_t n_pages) {
           if (e2 != cudaSuccess) return e2;
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_warp<R, 0>, 256, pc::kV6Smem);
         }
+        else if constexpr (Variant == 4) {
+          cudaError_t e2 = v9_opt_in<R>();
+          if (e2 != cudaSuccess) return e2;
+          return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_seeded<R>, 256, pc::kV9Smem);
+        }
         else
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
       }) != cudaSuccess)
@@ -227,7 +267,7 @@ unsigned pages_grid(size_t n_pages) {
   // v5 at ChaCha12 runs best at 2 of its 4 resident CTAs per SM: 2835 vs
   // 2774 GB/s through bench.py (profiles/r01_ctas_ab.txt) -- fewer
   // concurrent page streams, same ALU feed (ILP 4 per thread)
-  const int dflt = ((Variant == 2 || Variant == 3) && R == 12) ? std::min(occ, 2) : occ;
+  const int dflt = ((Variant == 2 || Variant == 3 || Variant == 4) && R == 12) ? std::min(occ, 2) : occ;
   const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : dflt;
   const uint64_t want = static_cast<uint64_t>(n_sm) * per_sm;
   const uint64_t slots = (n_pages + 3) / 4;
@@ -259,6 +299,27 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
         default: pc::k_crypt_pages_async<R, 3><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
       }
       counted();
+    }
+  }
+  else if (kern == 9) {
+    constexpr size_t kMax = size_t(1) << 30;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = seed_pool(dev);
+    v9_opt_in<R>();
+    for (size_t p0 = 0; p0 < n_pages; p0 += kMax) {
+      const uint32_t m = static_cast<uint32_t>(std::min(kMax, n_pages - p0));
+      pc::PageDesc dd{d.vaddrs ? d.vaddrs + p0 : nullptr, d.pids ? d.pids + p0 : nullptr,
+                      d.vaddr0 + 4096ull * p0, d.pid0};
+      uint4 *rec = nullptr;
+      if (!pool || cudaMallocFromPoolAsync(reinterpret_cast<void **>(&rec), size_t(m) * 64, pool, st) != cudaSuccess)
+        return; // the caller's cudaGetLastError reports it
+      pc::k_page_seed_table<<<(m + 255) / 256, 256, 0, st>>>(key, dd, rec, m);
+      counted();
+      pc::k_crypt_pages_seeded<R><<<pages_grid<R, 4>(m), 256, pc::kV9Smem, st>>>(key, rec, i4 + p0 * 256,
+                                                                                  o4 + p0 * 256, m);
+      counted();
+      cudaFreeAsync(rec, st);
     }
   }
   else if (kern == 6) {
@@ -370,7 +431,7 @@ int launch_crypt(const uint32_t *key, const pc::PageDesc &d, const void *in, voi
       default: return launch_tma_r<20>(key, d, in, out, n_pages, st);
     }
   }
-  if (kern == 2 || kern == 3 || kern == 5 || kern == 6) {
+  if (kern == 2 || kern == 3 || kern == 5 || kern == 6 || kern == 9) {
     switch (rounds) {
       case 8: launch_pages_r<8>(kern, key, d, in, out, n_pages, st); break;
       case 12: launch_pages_r<12>(kern, key, d, in, out, n_pages, st); break;
@@ -1651,6 +1712,7 @@ cudaError_t touch_rounds() {
   acc(v6_opt_in<R, 1>());
   acc(v6_opt_in<R, 2>());
   acc(v6_opt_in<R, 3>());
+  acc(v9_opt_in<R>());
   acc(touch(pc::k_keystream_seeds<R>));
   acc(touch(pc::k_service<R>));
   acc(touch(pc::k_slab_move<R, 0>));
@@ -1667,6 +1729,8 @@ extern "C" int pc_preload(int device) {
   CU(touch_rounds<12>());
   CU(touch_rounds<20>());
   CU(touch(pc::k_keygen));
+  CU(touch(pc::k_page_seed_table));
+  if (!seed_pool(device)) return fail(PC_ECUDA, "seed pool");
   CU(touch(pc::k_slab_wipe));
   CU(touch(pc::k_desc_check));
   CU(touch(pc::k_intpeak<0>));
@@ -2199,7 +2263,7 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "kernel")) {
-    if (value < 0 || value > 6) return fail(PC_EINVAL, "kernel must be 0 (auto) or 1..6");
+    if (value < 0 || (value > 6 && value != 9)) return fail(PC_EINVAL, "kernel must be 0 (auto), 1..6 or 9");
     t.kernel = static_cast<int>(value);
     return PC_OK;
   }

@@ -53,7 +53,7 @@ def knob():
 
 
 class TestDevicePath:
-    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6])
+    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 9])
     @pytest.mark.parametrize("rounds", [8, 12, 20])
     @pytest.mark.parametrize("n", [1, 3, 64, 4097])
     def test_contiguous_scalar_pid(self, dkey, n, rounds, kernel, knob):
@@ -66,7 +66,7 @@ class TestDevicePath:
         want = C.crypt_pages(KEY, None, None, pages, rounds=rounds, vaddr0=BASE, pid0=1, nthreads=8)
         assert np.array_equal(got.cpu().numpy(), want)
 
-    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6])
+    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 9])
     def test_per_page_descriptors(self, dkey, ref_pages, kernel, knob):
         import torch
 
@@ -88,7 +88,7 @@ class TestDevicePath:
     @pytest.mark.parametrize("shape", ["vaddr_array", "pid_array", "both"])
     @pytest.mark.parametrize("rounds", [8, 12, 20])
     @pytest.mark.parametrize("n", [1, 2, 3, 5, 1183, 2369, 4097])
-    @pytest.mark.parametrize("kernel", [0, 6])
+    @pytest.mark.parametrize("kernel", [0, 6, 9])
     def test_every_descriptor_shape_ragged(self, dkey, shape, rounds, n, kernel, knob):
         """Each descriptor shape compiles to its own loop (DM = vaddr array |
         pid array; page-pair loops for R <= 12 and for R = 20 with a vaddr
@@ -111,17 +111,18 @@ class TestDevicePath:
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=rounds, nthreads=8))
 
+    @pytest.mark.parametrize("kernel", [6, 9])
     @pytest.mark.parametrize("shape", ["contig", "vaddr_array", "pid_array", "both"])
     @pytest.mark.parametrize("rounds", [12, 20])
     @pytest.mark.parametrize("n", [75_777, 151_553])
-    def test_v6_many_table_refills(self, dkey, shape, rounds, n, knob):
+    def test_v6_many_table_refills(self, dkey, shape, rounds, n, kernel, knob):
         """k_crypt_pages_warp refills its per-slot seed table every 32 pages of
         a thread: batches long enough for several refills (n > 32 x the grid
         stride of 296/592 CTAs x 4 pages), ragged tails, every descriptor
         shape, random vaddrs whose high word changes."""
         import torch
 
-        knob("kernel", 6)
+        knob("kernel", kernel)
         rng = np.random.default_rng(n + rounds)
         pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
         va = (rng.integers(0, 2**52, size=n, dtype=np.uint64) << np.uint64(12))
@@ -130,11 +131,12 @@ class TestDevicePath:
         p_arg = t(pi.view(np.int32)) if shape in ("pid_array", "both") else 77
         v_ref = va if shape in ("vaddr_array", "both") else BASE + 4096 * np.arange(n, dtype=np.uint64)
         p_ref = pi if shape in ("pid_array", "both") else np.full(n, 77, np.uint32)
-        got = pc.crypt_pages(dkey, v_arg, p_arg, t(pages), rounds=rounds)
+        buf = t(pages)
+        got = pc.crypt_pages(dkey, v_arg, p_arg, buf, out=buf if kernel == 9 else None, rounds=rounds)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=rounds, nthreads=16))
 
-    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6])
+    @pytest.mark.parametrize("kernel", [1, 2, 3, 4, 5, 6, 9])
     def test_pid_per_page_variant(self, dkey, kernel, knob):
         """pid = 1 + (i % 64); also vaddr_hi changing mid-batch
         (the v2/v3 kernels cache the vaddr_hi/pid column rounds)."""
@@ -523,7 +525,7 @@ class TestEdgeShapes:
     def test_tiny_and_empty_device_batches_every_kernel(self, dkey, n, knob):
         import torch
 
-        for kernel in (1, 2, 3, 4, 5, 6):
+        for kernel in (1, 2, 3, 4, 5, 6, 9):
             knob("kernel", kernel)
             pages = rand_pages(n, 50 + n) if n else np.empty((0, 4096), np.uint8)
             got = pc.crypt_pages(dkey, BASE, 3, torch.from_numpy(pages).cuda())
