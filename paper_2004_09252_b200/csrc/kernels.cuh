@@ -542,11 +542,22 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     cp_async_wait<2>(); // this page's group has landed
     const uint4 *mine = &ring[st][tid * 4];
     const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
-    st_block<(ROUNDS <= 12)>(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
-                             d0.w ^ (x[3] + kSigma3)),
-             make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])),
-             make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
-             make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+    if constexpr (ROUNDS <= 12) {
+      st_block<true>(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                                     d0.w ^ (x[3] + kSigma3)),
+                     make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])),
+                     make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
+                     make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+    } else { // (each store right after its words: the schedule R=20 was tuned on)
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]),
+                              d3.w ^ (x[15] + b)));
+    }
     page += stride;
     if (page >= n_pages) break;
     dst += step;
@@ -600,11 +611,22 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     cp_async_wait<2>(); // this page's group has landed
     const uint4 *mine = &ring[st][tid * 4];
     const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
-    st_block<(ROUNDS <= 12)>(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
-                             d0.w ^ (x[3] + kSigma3)),
-             make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])),
-             make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
-             make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+    if constexpr (ROUNDS <= 12) {
+      st_block<true>(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                                     d0.w ^ (x[3] + kSigma3)),
+                     make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])),
+                     make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
+                     make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+    } else { // (each store right after its words: the schedule R=20 was tuned on)
+    st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)));
+    st_v4(dst + 1, make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]),
+                              d1.w ^ (x[7] + k[3])));
+    st_v4(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]),
+                              d2.w ^ (x[11] + k[7])));
+    st_v4(dst + 3, make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]),
+                              d3.w ^ (x[15] + b)));
+    }
       page += stride;
       if (page >= n_pages) return false;
       dst += step;
