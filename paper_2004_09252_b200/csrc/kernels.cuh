@@ -38,27 +38,16 @@ __device__ __forceinline__ void st_v4(uint4 *p, uint4 v) {
                : "memory");
 }
 
-// A thread's 64-byte block: four STG.128, or (WIDE) two 256-bit stores
-// (STG.E.ENL2.256, sm_100) -- half the store instructions on the MIO queue
-// the page stream shares with its cp.async copies and shared-memory reads.
-// v5 uses WIDE for ChaCha8/12, whose per-page descriptor loops are
-// MIO-limited (R=12 with pid + vaddr arrays 2620 -> 2670 GB/s); ChaCha20
-// contiguous loses with it (1779 -> 1745), profiles/r02_ab_st256.txt.
-template <bool WIDE>
-__device__ __forceinline__ void st_block(uint4 *p, uint4 a, uint4 b, uint4 c, uint4 d) {
-  if constexpr (WIDE) {
-    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
-                 "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-                 : "memory");
-    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p + 2), "r"(c.x), "r"(c.y), "r"(c.z),
-                 "r"(c.w), "r"(d.x), "r"(d.y), "r"(d.z), "r"(d.w)
-                 : "memory");
-  } else {
-    st_v4(p, a);
-    st_v4(p + 1, b);
-    st_v4(p + 2, c);
-    st_v4(p + 3, d);
-  }
+// 32 bytes with one 256-bit store (STG.E.ENL2.256, new on sm_100): v5 writes
+// a thread's 64-byte block with two of them at ChaCha8/12 -- half the store
+// instructions on the MIO queue the page stream shares with its cp.async
+// copies and shared-memory reads (R=12 with pid + vaddr arrays 2620 -> 2675
+// GB/s; contiguous unchanged; profiles/r02_ab_st256.txt).  ChaCha20 keeps
+// four STG.128.
+__device__ __forceinline__ void st_v8(uint4 *p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
+               "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
 }
 
 __device__ __forceinline__ void load_key(const uint32_t *__restrict__ key, uint32_t (&k)[8]) {
@@ -543,11 +532,11 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     const uint4 *mine = &ring[st][tid * 4];
     const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
     if constexpr (ROUNDS <= 12) {
-      st_block<true>(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
-                                     d0.w ^ (x[3] + kSigma3)),
-                     make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])),
-                     make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
-                     make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+      st_v8(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                            d0.w ^ (x[3] + kSigma3)),
+            make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])));
+      st_v8(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
+            make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
     } else { // (each store right after its words: the schedule R=20 was tuned on)
     st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
                           d0.w ^ (x[3] + kSigma3)));
@@ -612,11 +601,11 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
     const uint4 *mine = &ring[st][tid * 4];
     const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
     if constexpr (ROUNDS <= 12) {
-      st_block<true>(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
-                                     d0.w ^ (x[3] + kSigma3)),
-                     make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])),
-                     make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
-                     make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+      st_v8(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                            d0.w ^ (x[3] + kSigma3)),
+            make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])));
+      st_v8(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
+            make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
     } else { // (each store right after its words: the schedule R=20 was tuned on)
     st_v4(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
                           d0.w ^ (x[3] + kSigma3)));
