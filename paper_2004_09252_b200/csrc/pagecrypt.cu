@@ -20,6 +20,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <shared_mutex>
 #include <unordered_map>
 #include <string>
 #include <thread>
@@ -664,6 +665,7 @@ struct pc_key {
   pc_service *svc = nullptr; // resident workers for fault-sized host batches (pc_key_service)
   int svc_rounds = 0;
   int svc_workers = 0;
+  std::shared_mutex svc_mu;  // shared: a call using svc; exclusive: starting / stopping it
 };
 
 namespace {
@@ -1375,13 +1377,16 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
   if (vaddrs)
     for (size_t i = 0; i < n; ++i)
       if (vaddrs[i] & 4095) return fail(PC_EINVAL, "vaddr %#llx not page-aligned", (unsigned long long)vaddrs[i]);
-  if (!raw_key && key->svc && key->svc_rounds == rounds) {
+  if (!raw_key) {
     // fault-sized host batches on the key's resident workers: one ticket
-    // per page, spread over the workers, no launch
+    // per page, spread over the workers, no launch (the shared lock keeps a
+    // concurrent pc_key_service stop from freeing them under us)
+    std::shared_lock<std::shared_mutex> sl(const_cast<pc_key *>(key)->svc_mu);
     const int64_t lim = tuning().svc_pages.load();
     const size_t max_pages = lim > 0 ? static_cast<size_t>(lim) : 2 * static_cast<size_t>(key->svc_workers);
     int gin = -1, gout = -1;
-    if (n <= max_pages && !device_memory(in, &gin) && !device_memory(out, &gout))
+    if (key->svc && key->svc_rounds == rounds && n <= max_pages && !device_memory(in, &gin) &&
+        !device_memory(out, &gout))
       return crypt_on_service(key, vaddrs, pids, vaddr0, pid0, in, out, n);
   }
   std::lock_guard<std::mutex> lk(e->mu);
@@ -2112,7 +2117,7 @@ int pc_service_in_flight(pc_service *s, uint64_t *n) {
 int pc_key_service(pc_key *key, int n_workers, int rounds) {
   if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
   if (n_workers < 0) return fail(PC_EINVAL, "n_workers must be >= 0, got %d", n_workers);
-  std::lock_guard<std::mutex> lk(key->mu);
+  std::unique_lock<std::shared_mutex> xl(key->svc_mu);
   if (n_workers == 0) {
     if (!key->svc) return PC_OK;
     int rc = pc_service_stop(key->svc);

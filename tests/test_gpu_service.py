@@ -516,3 +516,46 @@ def test_key_service_small_host_batches_match_oracle(cuda, rounds):
         _native.tune("svc_pages", 0)
     dk.destroy()  # stops the workers first
     assert dk.destroyed
+
+
+def test_key_service_start_stop_beside_concurrent_calls(cuda):
+    """Four threads run 1-2 page crypt_pages calls under a key while a fifth
+    starts and stops the key's resident workers over and over: every result
+    equals the oracle (service or launch path, whichever was up) and no call
+    uses a stopped service."""
+    import paper_2004_09252_b200 as pc
+
+    key = bytes(range(90, 122))
+    dk = pc.DeviceKey.install(key, 0)
+    stop = threading.Event()
+    errors = []
+
+    def worker(seed):
+        rng = np.random.default_rng(seed)
+        try:
+            while not stop.is_set():
+                n = int(rng.integers(1, 3))
+                pages = rng.integers(0, 256, (n, 4096), dtype=np.uint8)
+                va = 0x5000_0000 + 4096 * int(rng.integers(0, 1 << 20))
+                want = C.crypt_pages(key, None, None, pages, vaddr0=va, pid0=seed)
+                got = pc.crypt_pages(dk, va, seed, pages)
+                if not np.array_equal(got, want):
+                    errors.append(f"mismatch seed {seed}")
+                    return
+        except Exception as exc:  # surfaced below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(s,)) for s in range(4)]
+    for t in threads:
+        t.start()
+    try:
+        for _ in range(15):
+            dk.start_service(n_workers=1)
+            stop.wait(0.02)
+            dk.stop_service()
+    finally:
+        stop.set()
+        for t in threads:
+            t.join()
+    dk.destroy()
+    assert not errors, errors[:3]
