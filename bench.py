@@ -528,7 +528,7 @@ def roofline(rounds, k_ms, bytes_per_step, peaks, n, kernel=None, desc=False):
         kernel = "k_crypt_pages_coalesced<8>" if rounds == 8 else "k_crypt_pages_async<%d>" % rounds
     return {
         "bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
-        "frac": round(achieved / peak, 4), "traffic": None if desc else _ncu_traffic(rounds, n),
+        "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(rounds, n, desc),
         "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
                           "ncu --set full capture of this kernel at this size (not re-measured in this run)",
         "kernel": kernel, "launch_ms": round(k_ms, 4),
@@ -757,12 +757,12 @@ def _hbm_peak():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def _ncu_traffic(rounds: int, n_pages: int):
+def _ncu_traffic(rounds: int, n_pages: int, desc: bool = False):
     """dram read+write bytes per launch from the committed ncu --set full capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        e = d.get(f"chacha{rounds}")
+        e = d.get(f"chacha{rounds}" + ("_desc" if desc else ""))
         if e and e.get("pages") == n_pages:
             return e["dram_bytes"]
     except (OSError, ValueError):

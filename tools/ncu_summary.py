@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv  > profiles/rNN_launches.txt
     python tools/ncu_summary.py report gpurun_out/x.ncu-rep [...]  > profiles/rNN_ncu_full.json
+    python tools/ncu_summary.py traffic "<source>" chacha20=gpurun_out/c20.ncu-rep [...] > profiles/ncu_traffic.json
 """
 
 import collections
@@ -82,8 +83,54 @@ def report(paths):
     print(json.dumps(out, indent=1))
 
 
+def _num(v):
+    return float(str(v).split()[0].replace(",", ""))
+
+
+def traffic(source, specs):
+    """profiles/ncu_traffic.json from one --set full report per bench kernel:
+    specs = name=path.ncu-rep[:pages] (name as bench.py looks it up:
+    chacha20, chacha12_desc, ...)."""
+    out = {"source": source}
+    for spec in specs:
+        name, path = spec.split("=", 1)
+        pages = 262144
+        if ":" in path:
+            path, pg = path.rsplit(":", 1)
+            pages = int(pg)
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        h, units = rows[0], rows[1]
+        d = dict(zip(h, rows[2]))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = _num(d["dram__bytes_read.sum"]) * scale[units[h.index("dram__bytes_read.sum")]]
+        wr = _num(d["dram__bytes_write.sum"]) * scale[units[h.index("dram__bytes_write.sum")]]
+        dur = _num(d["gpu__time_duration.sum"]) * {"ns": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}.get(
+            units[h.index("gpu__time_duration.sum")], 1)
+        stalls = {}
+        for i, col in enumerate(h):
+            mm = STALL_RE.match(col)
+            if mm and rows[2][i] not in ("", "n/a"):
+                stalls[mm.group(1)] = _num(rows[2][i])
+        tot = sum(stalls.values()) or 1.0
+        out[name] = {
+            "kernel": re.sub(r"\(.*", "", d.get("Kernel Name", "")), "pages": pages,
+            "dram_bytes": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
+            "algorithmic_bytes": pages * 8192 + (12 * pages if name.endswith("_desc") else 0),
+            "duration_us": round(dur, 3),
+            "alu_pipe_pct": d.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+            "dram_throughput_pct": d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "registers": d.get("launch__registers_per_thread"), "grid": d.get("launch__grid_size"),
+            "sm_clock_ghz": d.get("sm__cycles_elapsed.avg.per_second"),
+            "stalls": {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -x[1])[:6]},
+        }
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3:])
     else:
         report(sys.argv[2:])

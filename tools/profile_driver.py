@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--pages", type=int, default=262144)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--intpeak", type=int, default=None)
+    ap.add_argument("--desc", action="store_true",
+                    help="per-page descriptor arrays: permuted vaddrs, pid = 1 + i % 64 (bench extras.desc)")
     a = ap.parse_args()
     if a.intpeak is not None:
         v = ctypes.c_double()
@@ -37,8 +39,15 @@ def main():
     pages = torch.randint(0, 256, (a.pages, 4096), dtype=torch.uint8, device="cuda")
     out = torch.empty_like(pages)
     with pc.DeviceKey.install(bytes(range(32)), 0) as k:
+        va, pid = 0x1_0000_0000, 1
+        if a.desc:
+            import numpy as np
+            n = a.pages
+            perm = np.random.default_rng(0).permutation(n).astype(np.uint64)
+            va = torch.from_numpy((0x1_0000_0000 + 4096 * perm).view(np.int64)).cuda()
+            pid = torch.from_numpy((1 + np.arange(n) % 64).astype(np.int32)).cuda()
         for _ in range(a.launches):
-            pc.crypt_pages(k, 0x1_0000_0000, 1, pages, out=out, rounds=a.rounds, check=False)
+            pc.crypt_pages(k, va, pid, pages, out=out, rounds=a.rounds, check=False)
         torch.cuda.synchronize()
     print("done")
 
