@@ -59,6 +59,11 @@ def main():
     engines = [pc.Engine(0, n_streams=3, chunk_pages=512) for _ in range(2)]
     pool = None if a.no_service else WorkerPool(n_workers=8, keysource=lambda n: KEY)
     store = DevicePageStore(1 << 15, dkey)
+    if not a.no_service:
+        # round 2: single faults on the store's resident worker, 1-2 page host
+        # calls on the key's resident workers -- beside all the launches
+        store.start_service()
+        dkey.start_service(n_workers=2)
     counts = {}
     errors = []
     lock = threading.Lock()
@@ -107,8 +112,8 @@ def main():
                     stream.synchronize()
                     assert np.array_equal(got.cpu().numpy(), want), "device batch"
                     bump("device_batch")
-                elif op == 1:  # host batch
-                    n = rng.choice([1, 64, 65, 5000])
+                elif op == 1:  # host batch (1-2 pages: the key's resident workers when they run)
+                    n = rng.choice([1, 2, 64, 65, 5000])
                     pages = nrng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
                     v0 = 4096 * rng.randrange(1 << 30)
                     want = C.crypt_pages(KEY, None, None, pages, vaddr0=v0, pid0=t, nthreads=2)
