@@ -632,6 +632,142 @@ k_crypt_pages_async(const uint32_t *__restrict__ key, PageDesc desc, const uint4
 }
 
 // ---------------------------------------------------------------------------
+// v5r: v5's ring and page loop for per-page descriptor arrays, with each page
+// slot walking a contiguous RUN of pages (slot s takes [s*L, s*L + L), L
+// even) instead of every (gridDim*4)-th page, so two consecutive pages'
+// descriptors are adjacent: one 16-byte load fetches both vaddrs and one
+// 8-byte load both pids.  Per page that halves the descriptor loads on the
+// MIO queue the page stream shares (v5 at ChaCha12 is MIO-limited with
+// descriptors, profiles/r02_desc_experiments.txt).  The pair for pages
+// (p+2, p+3) is loaded while (p, p+1) run.  Needs vaddrs 16-byte and pids
+// 8-byte aligned (the host checks; else v5).
+template <int ROUNDS, int DM>
+__global__ void __launch_bounds__(256, 3)
+k_crypt_pages_run(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out, uint32_t n_pages,
+                  uint32_t run) {
+  constexpr bool VA = (DM & 1) != 0, PA = (DM & 2) != 0;
+  constexpr RotMul rm{};
+  constexpr int kStages = 3;
+  __shared__ uint4 ring[kStages][256 * 4];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t b = tid & 63;
+  const uint32_t sw = (tid >> 1) & 3;
+  uint32_t page = (blockIdx.x * 4 + (tid >> 6)) * run; // run is even: every run starts on an even page
+  const uint32_t end = min(n_pages, page + run);
+  if (page >= end) return;
+  const uint32_t base0 = smem_u32(&ring[0][tid * 4]);
+  constexpr uint32_t kStageBytes = 256 * 4 * 16;
+  const uint4 *src_ahead = in + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint4 *dst = out + static_cast<uint64_t>(page) * 256 + b * 4;
+  uint32_t page_ahead = page;
+  auto issue = [&](int st) {
+    if (page_ahead < end) {
+      const uint32_t sdst = base0 + st * kStageBytes;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async16(sdst + 16 * (c ^ sw), src_ahead + c);
+    }
+    cp_async_commit();
+    page_ahead += 1;
+    src_ahead += 256;
+  };
+  issue(0);
+  issue(1);
+  uint32_t k[8];
+  load_key(key, k);
+  uint32_t c3a = kSigma3, c3b = k[3], c3c = k[7], c3d = b;
+  quarter_round<0>(c3a, c3b, c3c, c3d, rm);
+  uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
+  uint32_t cached_hi = 0;
+  bool cached = false;
+  if constexpr (!PA) {
+    c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = desc.pid0;
+    quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+  }
+  // descriptors of the pair (p, p+1); p + 1 may be past the batch on its last page
+  auto load_pair = [&](uint32_t p, uint4 &vv, uint2 &pp) {
+    if (p + 1 < n_pages) {
+      if constexpr (VA) vv = __ldg(reinterpret_cast<const uint4 *>(desc.vaddrs + p));
+      if constexpr (PA) pp = __ldg(reinterpret_cast<const uint2 *>(desc.pids + p));
+    } else if (p < n_pages) {
+      if constexpr (VA) {
+        const uint64_t v = __ldg(desc.vaddrs + p);
+        vv = make_uint4(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32), 0, 0);
+      }
+      if constexpr (PA) pp = make_uint2(__ldg(desc.pids + p), 0);
+    }
+  };
+  uint4 vcur = make_uint4(0, 0, 0, 0), vnext = vcur;
+  uint2 pcur = make_uint2(0, 0), pnext = pcur;
+  load_pair(page, vcur, pcur);
+  load_pair(page + 2, vnext, pnext);
+  int st = 0;
+  auto one_page = [&](uint32_t vlo, uint32_t vhi, uint32_t pid) -> bool {
+    uint32_t s[3];
+    s[0] = vlo;
+    s[1] = vhi;
+    s[2] = pid;
+    issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
+    if (!cached || s[1] != cached_hi) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = s[1];
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      cached_hi = s[1];
+      cached = true;
+    }
+    if constexpr (PA) {
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = s[2];
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+    }
+    uint32_t x[16];
+    x[0] = kSigma0; x[4] = k[0]; x[8] = k[4]; x[12] = s[0];
+    quarter_round<0>(x[0], x[4], x[8], x[12], rm);
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = c3a; x[7] = c3b; x[11] = c3c; x[15] = c3d;
+    diagonal_round<0>(x, rm);
+#pragma unroll
+    for (int r = 1; r < ROUNDS / 2; ++r) {
+      column_round<0>(x, rm);
+      diagonal_round<0>(x, rm);
+    }
+    cp_async_wait<2>(); // this page's group has landed
+    const uint4 *mine = &ring[st][tid * 4];
+    const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
+    st_v8(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                          d0.w ^ (x[3] + kSigma3)),
+          make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])));
+    st_v8(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
+          make_uint4(d3.x ^ (x[12] + s[0]), d3.y ^ (x[13] + s[1]), d3.z ^ (x[14] + s[2]), d3.w ^ (x[15] + b)));
+    page += 1;
+    if (page >= end) return false;
+    dst += 256;
+    st = st == 2 ? 0 : st + 1;
+    return true;
+  };
+  for (;;) {
+    uint32_t lo0, hi0, lo1, hi1, p0, p1;
+    if constexpr (VA) {
+      lo0 = vcur.x; hi0 = vcur.y; lo1 = vcur.z; hi1 = vcur.w;
+    } else {
+      const uint64_t v0 = desc.vaddr0 + (static_cast<uint64_t>(page) << 12);
+      const uint64_t v1 = v0 + 4096;
+      lo0 = static_cast<uint32_t>(v0); hi0 = static_cast<uint32_t>(v0 >> 32);
+      lo1 = static_cast<uint32_t>(v1); hi1 = static_cast<uint32_t>(v1 >> 32);
+    }
+    if constexpr (PA) {
+      p0 = pcur.x; p1 = pcur.y;
+    } else {
+      p0 = p1 = desc.pid0;
+    }
+    vcur = vnext;
+    pcur = pnext;
+    load_pair(page + 4, vnext, pnext); // two pages ahead of the pair after this one
+    if (!one_page(lo0, hi0, p0)) break;
+    if (!one_page(lo1, hi1, p1)) break;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // v6: v5's cp.async page ring with the per-page seed rounds computed once
 // per page instead of once per thread.
 //

@@ -82,11 +82,15 @@ int env_int(const char *name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
+#ifndef PC_RUN_MAX_R
+#define PC_RUN_MAX_R 12
+#endif
 // Tuning knobs (env defaults at first use, pc_tune() at run time).
 struct Tuning {
   std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
   std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
+  std::atomic<int> run_desc{1};        // v5 with descriptor arrays at R <= 12: contiguous runs per slot
   std::atomic<int64_t> svc_pages{0};   // host batches up to this many pages go to the key's resident
                                        // workers when it has them (pc_key_service); 0 = 2 per worker
   std::atomic<int> kernel{0};          // HBM kernel: 0 = auto (per rounds, below), 1 = k_crypt_blocks,
@@ -108,6 +112,7 @@ struct Tuning {
     kernel = env_int("PAGECRYPT_KERNEL", 0);
     host_mode = env_int("PAGECRYPT_HOST_MODE", 2);
     ctas_per_sm = env_int("PAGECRYPT_CTAS_PER_SM", 0);
+    run_desc = env_int("PAGECRYPT_RUN_DESC", 1);
     if (const char *v = std::getenv("PAGECRYPT_ROTMASK")) rot_mask = static_cast<uint32_t>(std::strtoul(v, nullptr, 0));
     small_mode = env_int("PAGECRYPT_SMALL_MODE", 1);
     small_max = static_cast<size_t>(env_int("PAGECRYPT_SMALL_MAX", 64));
@@ -293,7 +298,25 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
       const unsigned grid = pages_grid<R, 2>(m);
       const auto a = i4 + p0 * 256;
       const auto b = o4 + p0 * 256;
-      switch ((dd.vaddrs ? 1 : 0) | (dd.pids ? 2 : 0)) {
+      const int dm = (dd.vaddrs ? 1 : 0) | (dd.pids ? 2 : 0);
+      if constexpr (R <= PC_RUN_MAX_R) {
+        // descriptor arrays at ChaCha8/12: contiguous page runs per slot, so a
+        // page pair's descriptors are one 16-byte and one 8-byte load
+        if (dm && tuning().run_desc.load() && grid &&
+            (reinterpret_cast<uintptr_t>(dd.vaddrs) & 15) == 0 && (reinterpret_cast<uintptr_t>(dd.pids) & 7) == 0) {
+          const uint64_t slots = uint64_t(grid) * 4;
+          const uint32_t run = static_cast<uint32_t>((((m + slots - 1) / slots) + 1) & ~uint64_t(1));
+          const unsigned g = static_cast<unsigned>((m + uint64_t(run) * 4 - 1) / (uint64_t(run) * 4));
+          switch (dm) {
+            case 1: pc::k_crypt_pages_run<R, 1><<<g, 256, 0, st>>>(key, dd, a, b, m, run); break;
+            case 2: pc::k_crypt_pages_run<R, 2><<<g, 256, 0, st>>>(key, dd, a, b, m, run); break;
+            default: pc::k_crypt_pages_run<R, 3><<<g, 256, 0, st>>>(key, dd, a, b, m, run); break;
+          }
+          counted();
+          continue;
+        }
+      }
+      switch (dm) {
         case 0: pc::k_crypt_pages_async<R, 0><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
         case 1: pc::k_crypt_pages_async<R, 1><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
         case 2: pc::k_crypt_pages_async<R, 2><<<grid, 256, 0, st>>>(key, dd, a, b, m); break;
@@ -1713,6 +1736,11 @@ cudaError_t touch_rounds() {
   acc(touch(pc::k_crypt_pages_async<R, 1>));
   acc(touch(pc::k_crypt_pages_async<R, 2>));
   acc(touch(pc::k_crypt_pages_async<R, 3>));
+  if constexpr (R <= PC_RUN_MAX_R) {
+    acc(touch(pc::k_crypt_pages_run<R, 1>));
+    acc(touch(pc::k_crypt_pages_run<R, 2>));
+    acc(touch(pc::k_crypt_pages_run<R, 3>));
+  }
   acc(v6_opt_in<R, 0>()); // loads the module and sets the shared-memory opt-in
   acc(v6_opt_in<R, 1>());
   acc(v6_opt_in<R, 2>());
@@ -2257,6 +2285,11 @@ int pc_tune(const char *knob, int64_t value) {
       }
     return fail(PC_EINVAL, "rotmask %#llx is not a compiled variant", (unsigned long long)value);
   }
+  if (!std::strcmp(knob, "run_desc")) {
+    if (value != 0 && value != 1) return fail(PC_EINVAL, "run_desc must be 0 or 1");
+    t.run_desc = static_cast<int>(value);
+    return PC_OK;
+  }
   if (!std::strcmp(knob, "svc_pages")) {
     if (value < 0 || value > 64) return fail(PC_EINVAL, "svc_pages must be 0..64");
     t.svc_pages = value;
@@ -2306,6 +2339,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   if (!std::strcmp(knob, "rotmask")) *value = t.rot_mask;
   else if (!std::strcmp(knob, "small_mode")) *value = t.small_mode;
   else if (!std::strcmp(knob, "svc_pages")) *value = t.svc_pages.load();
+  else if (!std::strcmp(knob, "run_desc")) *value = t.run_desc.load();
   else if (!std::strcmp(knob, "small_max")) *value = static_cast<int64_t>(t.small_max.load());
   else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
   else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;

@@ -88,8 +88,9 @@ class TestDevicePath:
     @pytest.mark.parametrize("shape", ["vaddr_array", "pid_array", "both"])
     @pytest.mark.parametrize("rounds", [8, 12, 20])
     @pytest.mark.parametrize("n", [1, 2, 3, 5, 1183, 2369, 4097])
-    @pytest.mark.parametrize("kernel", [0, 6, 9])
-    def test_every_descriptor_shape_ragged(self, dkey, shape, rounds, n, kernel, knob):
+    @pytest.mark.parametrize("kernel", [0, 5, 6, 9])
+    @pytest.mark.parametrize("run_desc", [0, 1])
+    def test_every_descriptor_shape_ragged(self, dkey, shape, rounds, n, kernel, run_desc, knob):
         """Each descriptor shape compiles to its own loop (DM = vaddr array |
         pid array; page-pair loops for R <= 12 and for R = 20 with a vaddr
         array alone): ragged counts around the grid stride (296 or 444 CTAs
@@ -102,7 +103,10 @@ class TestDevicePath:
         va = (rng.integers(0, 2**52, size=n, dtype=np.uint64) << np.uint64(12))
         va[: n // 2] = 0xFFFF_F000 + 4096 * np.arange(n // 2, dtype=np.uint64)  # crosses 4 GiB
         pi = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        if run_desc == 0 and kernel not in (0, 5):
+            pytest.skip("run_desc only changes v5")
         knob("kernel", kernel)
+        knob("run_desc", run_desc)  # v5 at R <= 12: contiguous page runs per slot (pair descriptor loads)
         v_arg = t(va.view(np.int64)) if shape != "pid_array" else BASE
         p_arg = t(pi.view(np.int32)) if shape != "vaddr_array" else 77
         v_ref = va if shape != "pid_array" else BASE + 4096 * np.arange(n, dtype=np.uint64)
@@ -110,6 +114,29 @@ class TestDevicePath:
         got = pc.crypt_pages(dkey, v_arg, p_arg, t(pages), rounds=rounds)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=rounds, nthreads=8))
+
+    @pytest.mark.parametrize("rounds", [8, 12])
+    @pytest.mark.parametrize("offset", [0, 1])
+    def test_run_desc_alignment_fallback(self, dkey, rounds, offset, knob):
+        """v5's page-run loop loads a page pair's descriptors as one 16-byte
+        vaddr and one 8-byte pid load; arrays that start off that alignment
+        (a tensor view one element in) take the per-page loop.  Both equal
+        the oracle, with odd and even page counts."""
+        import torch
+
+        knob("kernel", 5)
+        knob("run_desc", 1)
+        for n in (1, 2, 7, 1184, 2371):
+            rng = np.random.default_rng(n + offset)
+            pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
+            va = rng.integers(0, 2**52, size=n + 1, dtype=np.uint64) << np.uint64(12)
+            pi = rng.integers(0, 2**32, size=n + 1, dtype=np.uint64).astype(np.uint32)
+            v_t = t(va.view(np.int64))[offset:offset + n]
+            p_t = t(pi.view(np.int32))[offset:offset + n]
+            got = pc.crypt_pages(dkey, v_t, p_t, t(pages), rounds=rounds)
+            torch.cuda.synchronize()
+            want = C.crypt_pages(KEY, va[offset:offset + n], pi[offset:offset + n], pages, rounds=rounds)
+            assert np.array_equal(got.cpu().numpy(), want), n
 
     @pytest.mark.parametrize("kernel", [6, 9])
     @pytest.mark.parametrize("shape", ["contig", "vaddr_array", "pid_array", "both"])
