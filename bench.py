@@ -568,7 +568,7 @@ def desc_leg(torch, args, timed, n, rank, world, dev, bytes_per_step, peaks, red
     for r in (20, 12, 8):
         ms = timed(r, steps, 3, desc=(vaddrs, pids), tag=f"desc{r}") / steps
         t = max_over_ranks(ms, device=red_dev)
-        kern = ("k_crypt_pages_coalesced<8,3>" if r == 8 else "k_crypt_pages_async<%d,3>" % r)
+        kern = {8: "k_crypt_pages_coalesced<8>", 12: "k_crypt_pages_run<12,3>", 20: "k_crypt_pages_async<20,3>"}[r]
         res[f"chacha{r}"] = {"value": round(world * bytes_per_step / (t / 1e3) / 1e9, 2), "unit": "GB/s",
                              "roofline": roofline(r, ms, bytes_per_step, peaks, n, kernel=kern, desc=True)}
     return res
