@@ -103,3 +103,26 @@ def test_own_arm_line_has_every_contract_key(cuda):
     assert e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 8192 * 4096 and e["value"] > 0
     assert d["gpu_launches"] >= d["steps"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_one_gpu_share_the_key_and_split_the_pages(cuda):
+    """The N>1 path on the one B200 here (test mode: both ranks on cuda:0,
+    gloo): bench.py --gpus 2 self-launches two ranks, rank 0 generates the key
+    on the device and rank 1 imports it over CUDA IPC, each rank ciphers its
+    page range, and the gathered ranges equal rank 0's single call."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--same-device",
+                        "--dist-backend", "gloo", "--steps", "3", "--warmup", "3", "--pages", "16384",
+                        "--sweep-gib", "0.25", "--sustain-s", "0.1", "--cpu-seconds", "0.2"],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpus_active"] == 1
+    assert "CUDA IPC" in d["config"]["key"]
+    sp = d["extras"]["split_parity"]
+    assert sp["ranks"] == 2 and sp["identical_to_single_call"] is True
+    sw = d["extras"]["sweep"]
+    assert sw["ranks"] == 2 and sw["device"]["roundtrip_ok"] and sw["host"]["roundtrip_ok"]
