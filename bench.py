@@ -425,7 +425,10 @@ def main() -> int:
             ms = timed(r, max(5, args.steps // 2), 3) / max(5, args.steps // 2)
             t = max_over_ranks(ms, device=red_dev)
             extras[f"chacha{r}"] = {"value": round(world * bytes_per_step / (t / 1e3) / 1e9, 2),
-                                    "unit": "GB/s", "roofline": roofline(r, ms, bytes_per_step, peaks, n)}
+                                    "unit": "GB/s", "roofline": roofline(r, ms, bytes_per_step, peaks, n),
+                                    "parity": "the reference is ChaCha20-only: reduced rounds are pinned by "
+                                              "published zero-key ChaCha8/12 blocks (tests/golden/rfc8439.json) "
+                                              "and the round-parameterised oracle restatement"}
         extras["desc"] = desc_leg(torch, args, timed, n, rank, world, dev, bytes_per_step, peaks, red_dev,
                                   max_over_ranks)
         extras["sustained"] = sustained_leg(args, step, stream, torch, _native, local_rank, kernel_ms, rl,
