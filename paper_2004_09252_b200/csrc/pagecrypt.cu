@@ -1361,9 +1361,10 @@ int crypt_large(pc_engine *e, const uint32_t *key, const uint64_t *vaddrs, const
 namespace {
 int svc_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const void *src, void *dst,
                const pc::SvcOp *op, uint64_t *ticket);
+constexpr size_t kSvcMaxPages = 64; // largest host batch crypt_on_service takes (its ticket array)
 int crypt_on_service(const pc_key *key, const uint64_t *vaddrs, const uint32_t *pids, uint64_t vaddr0,
                      uint32_t pid0, const void *in, void *out, size_t n) {
-  uint64_t tickets[64];
+  uint64_t tickets[kSvcMaxPages];
   const int W = key->svc_workers;
   for (size_t i = 0; i < n; ++i) {
     const uint64_t va = vaddrs ? vaddrs[i] : vaddr0 + 4096ull * i;
@@ -1406,7 +1407,8 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
     // concurrent pc_key_service stop from freeing them under us)
     std::shared_lock<std::shared_mutex> sl(const_cast<pc_key *>(key)->svc_mu);
     const int64_t lim = tuning().svc_pages.load();
-    const size_t max_pages = lim > 0 ? static_cast<size_t>(lim) : 2 * static_cast<size_t>(key->svc_workers);
+    const size_t max_pages = std::min<size_t>(kSvcMaxPages, lim > 0 ? static_cast<size_t>(lim)
+                                                                      : 2 * static_cast<size_t>(key->svc_workers));
     int gin = -1, gout = -1;
     if (key->svc && key->svc_rounds == rounds && n <= max_pages && !device_memory(in, &gin) &&
         !device_memory(out, &gout))
