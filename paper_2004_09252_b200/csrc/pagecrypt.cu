@@ -90,7 +90,9 @@ struct Tuning {
   std::atomic<uint32_t> rot_mask{0};   // ROTMASK of the crypt kernel (one of kRotMasks)
   std::atomic<int> small_mode{1};      // 0 = staged copies, 1 = zero-copy on mapped pinned memory
   std::atomic<size_t> small_max{64};   // host batches up to this many pages take the small path
-  std::atomic<int> run_desc{1};        // v5 with descriptor arrays at R <= 12: contiguous runs per slot
+  std::atomic<int> run_desc{1};
+  std::atomic<int> svc_bell_ops{1};    // a store's service: its tickets' slots ride in the doorbell line
+                                       // (0 = the workers read every op line: tests the fallback)        // v5 with descriptor arrays at R <= 12: contiguous runs per slot
   std::atomic<int64_t> svc_pages{0};   // host batches up to this many pages go to the key's resident
                                        // workers when it has them (pc_key_service); 0 = 2 per worker
   std::atomic<int> kernel{0};          // HBM kernel: 0 = auto (per rounds, below), 1 = k_crypt_blocks,
@@ -113,6 +115,7 @@ struct Tuning {
     host_mode = env_int("PAGECRYPT_HOST_MODE", 2);
     ctas_per_sm = env_int("PAGECRYPT_CTAS_PER_SM", 0);
     run_desc = env_int("PAGECRYPT_RUN_DESC", 1);
+    svc_bell_ops = env_int("PAGECRYPT_SVC_BELL_OPS", 1);
     if (const char *v = std::getenv("PAGECRYPT_ROTMASK")) rot_mask = static_cast<uint32_t>(std::strtoul(v, nullptr, 0));
     small_mode = env_int("PAGECRYPT_SMALL_MODE", 1);
     small_max = static_cast<size_t>(env_int("PAGECRYPT_SMALL_MAX", 64));
@@ -1785,7 +1788,7 @@ constexpr uint32_t kServiceMagic = 0x73766331u; // "svc1"
 
 int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key, pc::SvcSlot *slots,
                    uint4 *pages, uint32_t ring, const pc::SvcBell *bell, const uint32_t *stop, uint32_t *started,
-                   pc::SvcDev *dev, uint4 *hdr, const pc::SvcOp *ops) {
+                   pc::SvcDev *dev, uint4 *hdr, const pc::SvcOp *ops, uint4 *store_slab) {
   // direct: every worker polls its own doorbell; else one extra CTA is the dispatcher
   // auto (2): direct polling while few workers poll -- 8.6 vs 10.0 us per
   // 1-page request at 16 workers, but 148 pollers congest PCIe (11.2 us)
@@ -1794,9 +1797,9 @@ int service_launch(int rounds, int workers, cudaStream_t st, const uint32_t *key
   const unsigned grid = static_cast<unsigned>(workers) + (direct ? 0 : 1);
   const uint32_t nw = static_cast<uint32_t>(workers);
   switch (rounds) {
-    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops); break;
-    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops); break;
-    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops); break;
+    case 8: pc::k_service<8><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops, store_slab); break;
+    case 12: pc::k_service<12><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops, store_slab); break;
+    default: pc::k_service<20><<<grid, 64, 0, st>>>(key, slots, pages, ring, nw, bell, stop, started, dev, hdr, direct, ops, store_slab); break;
   }
   counted();
   CU(cudaGetLastError());
@@ -1852,6 +1855,7 @@ struct pc_service {
   pc::SvcDev *dev = nullptr;                          // device-memory doorbell mirror
   pc::SvcOp *h_ops = nullptr, *d_ops = nullptr;       // mapped pinned: per slot, a store op's line
   uint64_t key_serial = 0;                            // the key the workers hold (pc_key::serial)
+  uint4 *store_slab = nullptr;                        // a store's own service: its slab (pc_store_service)
   uint4 *hdr = nullptr;                               // forwarded headers, n_workers x ring
   // Host-side slot protocol.  Slot j of a worker carries tickets j, j+R, ...
   //   next[j]  = the ticket whose result is the next to be delivered in slot j
@@ -1880,7 +1884,19 @@ int pc_service_max_workers(int device, int *n) {
   return PC_OK;
 }
 
+} // extern "C"
+int service_start(const pc_key *key, int n_workers, int ring_slots, int rounds, void *store_slab,
+                  pc_service **out);
+extern "C" {
 int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int rounds, pc_service **out) {
+  return service_start(key, n_workers, ring_slots, rounds, nullptr, out);
+}
+} // extern "C"
+
+// store_slab: the slab of the store that owns this service (its workers then
+// take a store ticket's slots from the doorbell line), or NULL
+int service_start(const pc_key *key, int n_workers, int ring_slots, int rounds, void *store_slab,
+                  pc_service **out) {
   if (!out) return fail(PC_EINVAL, "out is NULL");
   *out = nullptr;
   if (!key || key->magic != kKeyMagic) return fail(PC_ESTATE, "not a live pc_key");
@@ -1957,7 +1973,8 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
 #undef CUS
   // the kernel reads the key once; it must be resident before we report success
   rc = service_launch(rounds, n_workers, s->st, key->d_words, s->d_slots, reinterpret_cast<uint4 *>(s->d_pages),
-                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev, s->hdr, s->d_ops);
+                      s->ring, s->d_bell, s->d_ctrl, s->d_ctrl + 64, s->dev, s->hdr, s->d_ops,
+                      static_cast<uint4 *>(store_slab));
   if (rc != PC_OK) return bail(rc);
   const auto t0 = std::chrono::steady_clock::now();
   volatile uint32_t *started = s->h_ctrl + 64;
@@ -1976,10 +1993,12 @@ int pc_service_start(const pc_key *key, int n_workers, int ring_slots, int round
     }
   }
   s->key_serial = key->serial;
+  s->store_slab = static_cast<uint4 *>(store_slab);
   g_services_on[s->device].fetch_add(1);
   *out = s;
   return PC_OK;
 }
+extern "C" {
 
 } // extern "C"
 
@@ -2053,6 +2072,15 @@ int svc_submit(pc_service *s, int worker, uint64_t vaddr, uint32_t pid, const vo
   while (count->load(std::memory_order_acquire) != static_cast<uint32_t>(t)) {
     if (++bspins > 64) std::this_thread::yield();
     else cpu_relax();
+  }
+  // a store's own service: the newest ticket's slots ride in the doorbell
+  // line (tagged with the ticket), written before the doorbell
+  if (s->store_slab) {
+    const __m128i o = op && tuning().svc_bell_ops.load() ? _mm_set_epi32(static_cast<int>(op->put_slot), static_cast<int>(op->get_slot),
+                                         static_cast<int>(op->evict_vaddr >> 32),
+                                         static_cast<int>((op->evict_vaddr & ~uint64_t(4095)) | pc::op_tag(t)))
+                         : _mm_setzero_si128();
+    _mm_store_si128(reinterpret_cast<__m128i *>(hb + 1), o);
   }
   // count, pid and vaddr in ONE aligned 16-byte store (atomic on x86-64
   // CPUs with AVX), so the dispatcher's 16-byte read never sees a count
@@ -2287,6 +2315,11 @@ int pc_tune(const char *knob, int64_t value) {
       }
     return fail(PC_EINVAL, "rotmask %#llx is not a compiled variant", (unsigned long long)value);
   }
+  if (!std::strcmp(knob, "svc_bell_ops")) {
+    if (value != 0 && value != 1) return fail(PC_EINVAL, "svc_bell_ops must be 0 or 1");
+    t.svc_bell_ops = static_cast<int>(value);
+    return PC_OK;
+  }
   if (!std::strcmp(knob, "run_desc")) {
     if (value != 0 && value != 1) return fail(PC_EINVAL, "run_desc must be 0 or 1");
     t.run_desc = static_cast<int>(value);
@@ -2342,6 +2375,7 @@ int pc_tune_get(const char *knob, int64_t *value) {
   else if (!std::strcmp(knob, "small_mode")) *value = t.small_mode;
   else if (!std::strcmp(knob, "svc_pages")) *value = t.svc_pages.load();
   else if (!std::strcmp(knob, "run_desc")) *value = t.run_desc.load();
+  else if (!std::strcmp(knob, "svc_bell_ops")) *value = t.svc_bell_ops.load();
   else if (!std::strcmp(knob, "small_max")) *value = static_cast<int64_t>(t.small_max.load());
   else if (!std::strcmp(knob, "kernel")) *value = t.kernel;
   else if (!std::strcmp(knob, "host_mode")) *value = t.host_mode;

@@ -110,6 +110,13 @@ struct alignas(64) SvcOp {
 };
 static_assert(sizeof(SvcOp) == 64, "one 64-byte line per ring slot");
 constexpr uint32_t kOpStore = 1, kOpGet = 2, kOpPut = 4;
+// The newest store ticket's slots also ride in the doorbell's line (the
+// 16 bytes after the bell: evict_vaddr | tag, get_slot, put_slot), so a
+// worker of a store's own service knows every address at the poll and starts
+// the HBM slab read and both keystreams while the page crosses PCIe.  tag =
+// ticket % 4095 + 1 (never 0: a crypt ticket zeroes the chunk); a chunk whose
+// tag is not the ticket's is stale and the worker reads the SvcOp line.
+__host__ __device__ constexpr uint32_t op_tag(uint64_t ticket) { return static_cast<uint32_t>(ticket % 4095) + 1; }
 
 // Device-side control block (device memory).
 // Host doorbell of one worker (mapped pinned memory, 16 bytes, written by
@@ -152,9 +159,10 @@ template <int ROUNDS>
 __global__ void __launch_bounds__(64, 1)
 k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32_t ring, uint32_t n_workers,
           const SvcBell *host_bell, const uint32_t *host_stop, uint32_t *started, SvcDev *dev,
-          uint4 *hdr, uint32_t direct, const SvcOp *ops) {
+          uint4 *hdr, uint32_t direct, const SvcOp *ops, uint4 *store_slab) {
   __shared__ uint4 tile[256]; // one 4 KiB page
   __shared__ uint4 bell_s;    // direct mode: the doorbell thread 0 saw (count, pid, vaddr)
+  __shared__ uint4 op_s;      // ... and the store-op chunk of its line
   const uint32_t lane = threadIdx.x;
   if (blockIdx.x == n_workers) {
     if (threadIdx.x >= 32) return;
@@ -244,6 +252,7 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
   SvcSlot *myring = slots + static_cast<uint64_t>(worker) * ring;
   uint4 *mypages = pages + static_cast<uint64_t>(worker) * ring * 256;
   uint4 seen_bell = make_uint4(0, 0, 0, 0); // direct mode: last doorbell read (count, pid, vaddr)
+  uint4 seen_op = make_uint4(0, 0, 0, 0);   // direct mode: the op chunk read with it
   for (uint64_t head = 0;; ++head) {
     uint4 hd;
     if (direct) {
@@ -252,8 +261,11 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
       // rides in the doorbell
       if (seen_bell.x == static_cast<uint32_t>(head)) { // nothing published beyond head yet
         if (tid == 0) {
-          uint4 b;
+          uint4 b, o;
           for (uint32_t polls = 1;; ++polls) {
+            // the op chunk is read beside the doorbell (not ordered after it:
+            // its tag says whether it belongs to the newest ticket)
+            o = ld_volatile_v4(reinterpret_cast<const uint4 *>(host_bell + worker * kBellStride + 1));
             // acquire: the page reads below are ordered after the doorbell
             b = ld_acquire_sys_v4(reinterpret_cast<const uint4 *>(host_bell + worker * kBellStride));
             if (b.x != static_cast<uint32_t>(head)) break;
@@ -264,9 +276,11 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
             }
           }
           bell_s = b;
+          op_s = o;
         }
         named_bar(64);
         seen_bell = bell_s;
+        seen_op = op_s;
         named_bar(64); // bell_s may be rewritten by the next request
         if (seen_bell.x == static_cast<uint32_t>(head)) return; // stop
       }
@@ -306,18 +320,32 @@ k_service(const uint32_t *__restrict__ key, SvcSlot *slots, uint4 *pages, uint32
     uint32_t x[16];
     if (op & kOpStore) {
       // ---- store op: refault (slab -> ring page) and/or evict (ring page -> slab)
-      const uint4 *oh = reinterpret_cast<const uint4 *>(ops + static_cast<uint64_t>(worker) * ring + head % ring);
-      const uint4 h0 = ld_volatile_v4(oh), h1 = ld_volatile_v4(oh + 1); // one PCIe read per warp
-      if (op & kOpGet) { // the refault keystream is computed while the op line crosses PCIe
-        const uint32_t sd[4] = {static_cast<uint32_t>(vaddr), static_cast<uint32_t>(vaddr >> 32), pid, tid};
-        chacha_block<ROUNDS, 0>(x, k, sd, rm);
+      uint4 h0, h1; // {slab lo, slab hi, evict lo, evict hi}, {get_slot, put_slot, -, -}
+      const bool in_bell = store_slab && direct && hd.w == static_cast<uint32_t>(head) &&
+                           (seen_op.x & 4095u) == op_tag(head);
+      if (in_bell) { // every address came with the doorbell: no op-line round trip
+        const uint64_t sp = reinterpret_cast<uint64_t>(store_slab);
+        h0 = make_uint4(static_cast<uint32_t>(sp), static_cast<uint32_t>(sp >> 32), seen_op.x & ~4095u, seen_op.y);
+        h1 = make_uint4(seen_op.z, seen_op.w, 0, 0);
+      } else {
+        const uint4 *oh = reinterpret_cast<const uint4 *>(ops + static_cast<uint64_t>(worker) * ring + head % ring);
+        h0 = ld_volatile_v4(oh); // one PCIe read per warp
+        h1 = ld_volatile_v4(oh + 1);
       }
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : : "memory");
       uint4 *slab = reinterpret_cast<uint4 *>(static_cast<uint64_t>(h0.x) | (static_cast<uint64_t>(h0.y) << 32));
       uint4 *gblk = slab + static_cast<uint64_t>(h1.x) * 256 + 4 * tid; // this thread's 64-byte block
       uint4 *pblk = slab + static_cast<uint64_t>(h1.y) * 256 + 4 * tid;
       uint4 c[4];
-      if (op & kOpGet) {
+      if (in_bell && (op & kOpGet)) { // the HBM slab read goes out before the keystream, too
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = gblk[j];
+      }
+      if (op & kOpGet) { // the refault keystream is computed while the loads are in flight
+        const uint32_t sd[4] = {static_cast<uint32_t>(vaddr), static_cast<uint32_t>(vaddr >> 32), pid, tid};
+        chacha_block<ROUNDS, 0>(x, k, sd, rm);
+      }
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : : "memory");
+      if (!in_bell && (op & kOpGet)) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) c[j] = gblk[j];
       }

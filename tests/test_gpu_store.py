@@ -338,12 +338,25 @@ def test_out_of_range_vaddrs_never_alias_stored_pages(dkey):
     s.close()
 
 
+@pytest.fixture
+def bell_ops():
+    """Set the svc_bell_ops knob for one test (1: a store ticket's slots ride
+    in the doorbell line; 0: the workers read the op line, the fallback)."""
+    from paper_2004_09252_b200 import _native
+
+    saved = _native.tune_get("svc_bell_ops")
+    yield lambda v: _native.tune("svc_bell_ops", v)
+    _native.tune("svc_bell_ops", saved)
+
+
+@pytest.mark.parametrize("in_bell", [1, 0], ids=["slots_in_doorbell", "op_line"])
 @pytest.mark.parametrize("rounds", [8, 12, 20])
-def test_service_faults_match_launch_faults(dkey, rounds):
+def test_service_faults_match_launch_faults(dkey, rounds, in_bell, bell_ops):
     """A random fault stream (refault + eviction, refault only, eviction only,
     first touch) through the resident worker gives the same outputs, the
     same stored ciphertext (== the oracle's) and the same free-slot count as
     the same stream through pc_store_swap launches."""
+    bell_ops(in_bell)
     rng = np.random.default_rng(rounds)
     stores = [DevicePageStore(40, dkey, rounds=rounds) for _ in range(2)]
     stores[1].start_service()
