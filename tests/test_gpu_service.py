@@ -564,17 +564,24 @@ def test_key_service_start_stop_beside_concurrent_calls(cuda):
 def test_key_service_many_workers_batch_limit(cuda):
     """With 40 resident workers (past the direct-polling limit: the
     dispatcher forwards the doorbells) the service takes host batches up to
-    its 64-ticket limit -- 2 per worker would be 80 -- and larger ones launch;
-    both equal the oracle."""
+    6 pages by default (each ticket costs the host ~1.2 us, so from ~8 pages
+    one launch is faster) and up to the knob svc_pages (<= 64, its ticket
+    array) when set; larger batches launch; all equal the oracle."""
     import paper_2004_09252_b200 as pc
 
     key = bytes(range(130, 162))
     rng = np.random.default_rng(5)
     with pc.DeviceKey.install(key, 0) as dk:
         dk.start_service(n_workers=40)
-        for n, launches in ((64, False), (70, True)):
-            pages = rng.integers(0, 256, (n, 4096), dtype=np.uint8)
-            before = _native.tune_get("launches")
-            got = pc.crypt_pages(dk, 0x8000_0000, 17, pages)
-            assert (_native.tune_get("launches") > before) == launches, n
-            assert np.array_equal(got, C.crypt_pages(key, None, None, pages, vaddr0=0x8000_0000, pid0=17))
+        cases = [(None, 6, False), (None, 7, True), (64, 64, False), (64, 70, True)]
+        saved = _native.tune_get("svc_pages")
+        try:
+            for knob, n, launches in cases:
+                _native.tune("svc_pages", 0 if knob is None else knob)
+                pages = rng.integers(0, 256, (n, 4096), dtype=np.uint8)
+                before = _native.tune_get("launches")
+                got = pc.crypt_pages(dk, 0x8000_0000, 17, pages)
+                assert (_native.tune_get("launches") > before) == launches, (knob, n)
+                assert np.array_equal(got, C.crypt_pages(key, None, None, pages, vaddr0=0x8000_0000, pid0=17))
+        finally:
+            _native.tune("svc_pages", saved)
