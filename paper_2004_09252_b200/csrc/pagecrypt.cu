@@ -273,10 +273,12 @@ unsigned pages_grid(size_t n_pages) {
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages<R>, 256, 0);
       }) != cudaSuccess)
     return 0; // the launch then fails loudly ("invalid configuration")
-  // v5 at ChaCha12 runs best at 2 of its 4 resident CTAs per SM: 2835 vs
-  // 2774 GB/s through bench.py (profiles/r01_ctas_ab.txt) -- fewer
-  // concurrent page streams, same ALU feed (ILP 4 per thread)
-  const int dflt = ((Variant == 2 || Variant == 3 || Variant == 4) && R == 12) ? std::min(occ, 2) : occ;
+  // v5 at ChaCha12 runs best below its 4 resident CTAs per SM: round 1, 2
+  // CTAs: 2835 vs 2774 GB/s (profiles/r01_ctas_ab.txt) -- fewer concurrent
+  // page streams, same ALU feed (ILP 4 per thread); with the 256-bit stores
+  // (round 2) 3 CTAs: 2853 vs 2845 contiguous, 2747-2751 vs 2692-2746 with
+  // descriptor arrays (profiles/r02_ctas_r12.txt)
+  const int dflt = ((Variant == 2 || Variant == 3 || Variant == 4) && R == 12) ? std::min(occ, 3) : occ;
   const int per_sm = tuning().ctas_per_sm.load() > 0 ? tuning().ctas_per_sm.load() : dflt;
   const uint64_t want = static_cast<uint64_t>(n_sm) * per_sm;
   const uint64_t slots = (n_pages + 3) / 4;
