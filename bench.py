@@ -797,7 +797,7 @@ def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
     # 1-2 page batches become service tickets instead of launches
     dk = pc.DeviceKey.generate(device)
     try:
-        dk.start_service(n_workers=2)
+        dk.start_service(n_workers=4)
         res["resident_workers"] = {}
         for n in (1, 2, 4):
             src = torch.randint(0, 256, (n, PAGE), dtype=torch.uint8).pin_memory()
@@ -813,7 +813,7 @@ def latency_sweep(pc, key, device: int, reps: int = 1000) -> dict:
             p50 = ts[len(ts) // 2] / 1e3
             res["resident_workers"][str(n)] = {"p50_us": round(p50, 2),
                                                "p99_us": round(ts[int(len(ts) * 0.99)] / 1e3, 2)}
-        res["resident_workers"]["workers"] = 2
+        res["resident_workers"]["workers"] = 4
     finally:
         dk.destroy()
     return res

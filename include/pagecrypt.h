@@ -198,7 +198,7 @@ int pc_service_stop(pc_service *svc);
 /* key service: start (n_workers > 0) or stop (0) resident workers holding
  * `key` (this section's kernel).  While they run, pc_crypt_pages_host calls
  * under `key` with `rounds` on at most svc_pages host pages (pc_tune knob;
- * 0 = 2 per worker, at most 6) are one service ticket per page instead of a launch --
+ * 0 = one per worker, at most 6) are one service ticket per page instead of a launch --
  * the fault handler's 1-2 page calls (orchestrator.py:197-198,234-235) skip
  * the launch and stream sync.  pc_key_destroy stops them. */
 int pc_key_service(pc_key *key, int n_workers, int rounds);

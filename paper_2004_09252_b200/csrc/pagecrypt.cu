@@ -94,7 +94,7 @@ struct Tuning {
   std::atomic<int> svc_bell_ops{1};    // a store's service: its tickets' slots ride in the doorbell line
                                        // (0 = the workers read every op line: tests the fallback)        // v5 with descriptor arrays at R <= 12: contiguous runs per slot
   std::atomic<int64_t> svc_pages{0};   // host batches up to this many pages go to the key's resident
-                                       // workers when it has them (pc_key_service); 0 = 2 per worker, <= 6
+                                       // workers when it has them (pc_key_service); 0 = 1 per worker, <= 6
   std::atomic<int> kernel{0};          // HBM kernel: 0 = auto (per rounds, below), 1 = k_crypt_blocks,
                                        // 2 = k_crypt_pages, 3 = k_crypt_pages_coalesced,
                                        // 4 = k_crypt_pages_tma, 5 = k_crypt_pages_async,
@@ -1412,11 +1412,12 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
     // concurrent pc_key_service stop from freeing them under us)
     std::shared_lock<std::shared_mutex> sl(const_cast<pc_key *>(key)->svc_mu);
     const int64_t lim = tuning().svc_pages.load();
-    // auto: 2 per worker, at most 6 -- each ticket costs the host ~1.2 us of
-    // copies and doorbell work, so from ~8 pages on one launch is faster
+    // auto: one page per worker, at most 6 -- each ticket costs the host
+    // ~1.2 us of copies and doorbell work, and a worker's second ticket waits
+    // for its first, so beyond that one launch is faster
     // (profiles/r02_key_service_sweep.json)
     const size_t max_pages = std::min<size_t>(
-        kSvcMaxPages, lim > 0 ? static_cast<size_t>(lim) : std::min<size_t>(6, 2 * static_cast<size_t>(key->svc_workers)));
+        kSvcMaxPages, lim > 0 ? static_cast<size_t>(lim) : std::min<size_t>(6, static_cast<size_t>(key->svc_workers)));
     int gin = -1, gout = -1;
     if (key->svc && key->svc_rounds == rounds && n <= max_pages && !device_memory(in, &gin) &&
         !device_memory(out, &gout))

@@ -174,7 +174,7 @@ class DeviceKey:
 
     def start_service(self, n_workers: int = 1, rounds: int = 20) -> None:
         """Start resident GPU workers holding this key (``pc_key_service``):
-        host batches of up to 2 pages per worker (at most 6) under this key and round
+        host batches of up to one page per worker (at most 6) under this key and round
         count then run as service tickets instead of launches -- the fault
         handler's 1-2 page calls skip the launch and the stream sync.
         ``stop_service``/``destroy`` stop them."""

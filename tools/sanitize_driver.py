@@ -87,8 +87,8 @@ def main():
         st.close()
         # 1-2 page host calls on the key's resident workers (pc_key_service)
         print("key service", flush=True)
-        k.start_service(n_workers=2)
-        for m in (1, 2, 4):  # <= 2 pages per worker: every call is service tickets, no launch
+        k.start_service(n_workers=4)
+        for m in (1, 2, 4):  # <= 1 page per worker: every call is service tickets, no launch
             got = pc.crypt_pages(k, 0x4000, 6, pages[:m])
             assert np.array_equal(got, C.crypt_pages(KEY, None, None, pages[:m], vaddr0=0x4000, pid0=6))
         k.stop_service()
