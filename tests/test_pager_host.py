@@ -235,3 +235,72 @@ def test_clients_are_isolated():
         assert {k: c for k, c in store.ct.items() if k[0] == cl} == s_store.ct
         a, b = pager.metrics[cl], s_pager.metrics[cl]
         assert (a.faults, a.evictions, a.decrypt_ops, a.encrypt_ops) == (b.faults, b.evictions, b.decrypt_ops, b.encrypt_ops)
+
+
+class NativeFakeStore(FakeStore):
+    """FakeStore plus DevicePageStore.fault (pc_store_fault's contract): the
+    pager then resolves a single fault as one native call."""
+
+    def fault(self, client, vaddr, out, evict_vaddr=None, evict_plain=None):
+        self.calls.append(("fault", evict_plain is not None))
+        self._maybe_fail("fault")
+        assert out.dtype == np.uint8 and out.size == 4096
+        if evict_plain is not None:
+            assert isinstance(evict_plain, np.ndarray) and evict_plain.dtype == np.uint8
+            assert evict_plain.size == 4096 and evict_plain.flags.c_contiguous
+            if (client, evict_vaddr) in self.ct and evict_vaddr != vaddr:
+                raise ContractViolation("duplicate store insert")
+        hit = (client, vaddr) in self.ct
+        if hit:
+            out[:] = np.frombuffer(O.crypt_page(KEY, vaddr, client.pid, self.ct.pop((client, vaddr))), np.uint8)
+        if evict_plain is not None:
+            self.ct[(client, evict_vaddr)] = O.crypt_page(KEY, evict_vaddr, client.pid, evict_plain.tobytes())
+        return hit
+
+
+@pytest.mark.parametrize("W", [1, 4])
+def test_native_single_faults_match_reference_semantics(W):
+    """Single faults through the store's one-call fault (the resident-worker
+    path on a GPU) give the reference orchestrator's results; the client's
+    page handed to the eviction is not modified (the library copies it)."""
+    store = NativeFakeStore()
+    mem = {}
+    handed = []
+
+    def fetch(client, vaddrs):
+        page = np.frombuffer(mem.pop(vaddrs[0]), np.uint8).copy()
+        handed.append((page, page.copy()))
+        return page  # one page as is (the bench's client)
+
+    pager = WindowPager(store, fetch, window_capacity=W)
+    pager.register(C)
+    model = Model(W)
+    rng = random.Random(W)
+    pages = [0x20000 + 4096 * i for i in range(12)]
+    for _ in range(200):
+        resident = set(pager.window(C))
+        v = rng.choice([p for p in pages if p not in resident])
+        got = pager.fault(C, v)
+        assert [got] == model.batch([v])
+        mem[v] = scribble(v, got)
+    assert all(np.array_equal(a, b) for a, b in handed)
+    assert {k[1]: c for k, c in store.ct.items()} == model.store
+    assert all(c[0] == "fault" for c in store.calls)
+
+
+def test_native_fault_converts_and_checks_the_evicted_page():
+    """fetch_evicted may hand back any array-like of the page's 4096 byte
+    values (a private uint8 copy is made, and wiped); a wrong size is a
+    ContractViolation and the window is left as it was."""
+    store = NativeFakeStore()
+    mem = {}
+    pager = WindowPager(store, lambda c, vs: mem.pop(vs[0]), window_capacity=1)
+    pager.register(C)
+    pager.fault(C, 0x1000)
+    mem[0x1000] = np.arange(4096, dtype=np.int64) % 256  # int64 values, not uint8 bytes
+    pager.fault(C, 0x2000)  # evicts 0x1000
+    assert store.ct[(C, 0x1000)] == O.crypt_page(KEY, 0x1000, C.pid, (np.arange(4096) % 256).astype(np.uint8).tobytes())
+    mem[0x2000] = np.zeros(100, np.uint8)
+    with pytest.raises(ContractViolation):
+        pager.fault(C, 0x3000)
+    assert pager.window(C) == [0x2000]
