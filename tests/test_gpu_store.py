@@ -428,3 +428,54 @@ def test_service_fault_errors_leave_store_unchanged(dkey):
     with pytest.raises(PageCryptError):
         keyless.start_service()
     keyless.close()
+
+
+def test_store_service_start_stop_beside_concurrent_faults(dkey):
+    """Three threads fault their own clients' pages through one store while a
+    fourth starts and stops the store's resident worker over and over: every
+    refault returns what was evicted (oracle-checked ciphertext in between),
+    whichever path -- ticket or launch -- served it."""
+    import threading
+
+    s = DevicePageStore(256, dkey)
+    stop = threading.Event()
+    errors = []
+
+    def worker(t):
+        rng = np.random.default_rng(t)
+        c = ClientId(500 + t, 0)
+        held = {}  # vaddr -> plaintext the client holds
+        stored = {}  # vaddr -> plaintext evicted into the store
+        try:
+            while not stop.is_set():
+                v = 0x4000_0000 + 4096 * int(rng.integers(0, 24))
+                if v in held:
+                    continue
+                out = np.zeros(4096, np.uint8)
+                ev = next(iter(held)) if len(held) >= 4 else None
+                plain = None if ev is None else np.frombuffer(held[ev], np.uint8).copy()
+                hit = s.fault(c, v, out, ev, plain)
+                if hit != (v in stored) or (hit and out.tobytes() != stored.pop(v)):
+                    errors.append(f"thread {t}: wrong refault of {v:#x}")
+                    return
+                if ev is not None:
+                    stored[ev] = held.pop(ev)
+                held[v] = rng.bytes(4096)
+        except Exception as exc:
+            errors.append(f"thread {t}: {exc!r}")
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(3)]
+    for th in threads:
+        th.start()
+    try:
+        for _ in range(12):
+            s.start_service()
+            stop.wait(0.03)
+            s.stop_service()
+            stop.wait(0.01)
+    finally:
+        stop.set()
+        for th in threads:
+            th.join()
+    s.close()
+    assert not errors, errors[:3]
