@@ -288,10 +288,14 @@ int pc_host_unregister(void *p);
 int pc_intpeak(int device, int kind, double *ops_per_s);
 /* Process-wide knobs: "rotmask" (compiled FMA-pipe rotate pattern of the
  * crypt kernel, see chacha.cuh), "small_mode" (0 staged copies / 1 zero-copy
- * for small host batches), "small_max", "kernel" (0 auto, 1..5 page-kernel
+ * for small host batches), "small_max", "kernel" (0 auto, 1..6 or 9 page-kernel
  * variant), "host_mode" (0..3 host pipeline), "ctas_per_sm", "dev_direct",
- * "peer_direct" (device-memory endpoints, see (v)); pc_tune_get
- * also reads "launches", the number of kernels this library has launched. */
+ * "peer_direct" (device-memory endpoints, see (v)), "svc_direct" (0/1/2 auto:
+ * worker service doorbell polling), "run_desc" (1: descriptor arrays at
+ * ChaCha8/12 walk contiguous page runs per slot), "svc_pages" (key service
+ * batch limit, 0 auto), "svc_bell_ops" (1: a store service's ticket slots
+ * ride in the doorbell line); pc_tune_get also reads "launches", the number
+ * of kernels this library has launched. */
 int pc_tune(const char *knob, int64_t value);
 int pc_tune_get(const char *knob, int64_t *value);
 
