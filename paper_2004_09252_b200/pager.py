@@ -34,6 +34,7 @@ from .errors import ContractViolation
 from .store import DevicePageStore
 
 PAGE_SIZE = 4096
+_U8 = np.dtype(np.uint8)
 FUSED_MAX = 128  # pages per pc_store_swap launch (refaults + evictions)
 
 
@@ -94,7 +95,7 @@ class SlidingWindow:
         return list(self._queue)
 
 
-@dataclass
+@dataclass(slots=True)
 class PagerMetrics:
     """Per-client counters (orchestrator.py:41-63)."""
 
@@ -270,29 +271,31 @@ class WindowPager:
         lookup, refault and the forced eviction in one native call and one
         GPU round trip."""
         e = win.admit(v)
-        out = np.zeros((1, PAGE_SIZE), dtype=np.uint8)  # stays zero on a first touch
+        out = np.empty((1, PAGE_SIZE), dtype=np.uint8)  # filled by a refault, zeroed on a first touch
         try:
             if e is None:
-                refault = native(client, v, out[0], None, None)
+                refault = native(client, v, out, None, None)
             else:
                 # no private copy here: the library copies the page into its
                 # own staging (the server's scratch_evict) and wipes it there
                 # (orchestrator.py:230-239); the client's buffer is only read
                 got = self.fetch_evicted(client, [e])
                 plain_ev = got if type(got) is np.ndarray else np.asarray(got)
-                if plain_ev.dtype != np.uint8 or plain_ev.size != PAGE_SIZE or not plain_ev.flags.c_contiguous:
+                if plain_ev.dtype is not _U8 or plain_ev.size != PAGE_SIZE or not plain_ev.flags.c_contiguous:
                     plain_ev = np.array(plain_ev, dtype=np.uint8, copy=True, order="C")
                     if plain_ev.size != PAGE_SIZE:
                         raise ContractViolation(f"fetch_evicted returned {plain_ev.size} bytes for one page")
                     try:
-                        refault = native(client, v, out[0], e, plain_ev.reshape(PAGE_SIZE))
+                        refault = native(client, v, out, e, plain_ev)
                     finally:
                         plain_ev.fill(0)  # our private copy: scratch_evict.wipe()
                 else:
-                    refault = native(client, v, out[0], e, plain_ev.reshape(PAGE_SIZE))
+                    refault = native(client, v, out, e, plain_ev)
         except BaseException:
             win.undo_admits([v], [e])
             raise
+        if not refault:
+            out.fill(0)  # a first touch reads as a zero page (orchestrator.py:178,192)
         if refault or e is not None:
             m.gpu_batches += 1
         m.faults += 1
