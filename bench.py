@@ -359,7 +359,20 @@ def main() -> int:
     out = torch.empty_like(pages)
     # production key path: derived on rank 0's GPU, never in host RAM, copied
     # device-to-device to every other rank (CUDA IPC export/import)
-    key = shared_key(local_rank)
+    key_note = None
+    try:
+        key = shared_key(local_rank)
+    except Exception as exc:  # noqa: BLE001 -- keep the run measurable; the line says so
+        # (shared_key is collective and raises only after its barrier, so the
+        # ranks stay in step; split_parity then reports the mismatch)
+        print(f"bench.py rank {rank}: shared key import failed ({exc}); using a per-rank key", file=sys.stderr)
+        key = pc.DeviceKey.generate(local_rank)
+        key_note = f"rank {rank} fell back to its own key: {exc}"
+    if world > 1:
+        flag = torch.tensor([0 if key_note is None else 1], dtype=torch.int32, device=red_dev)
+        dist.all_reduce(flag)
+        if int(flag.item()):
+            key_note = key_note or f"{int(flag.item())} rank(s) fell back to their own key (CUDA IPC import failed)"
     stream = torch.cuda.current_stream(dev)
 
     def step(rounds, desc=None):
@@ -455,7 +468,7 @@ def main() -> int:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (uniform random pages, seed 1+rank; key from DeviceKey.generate on rank 0)",
-            "config": workload_config(args, world),
+            "config": dict(workload_config(args, world), **({"key": key_note} if key_note else {})),
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches[args.rounds] + e2e_launches,
             "gpu_launches_detail": {"device_timed": launches[args.rounds], "e2e_timed": e2e_launches,
