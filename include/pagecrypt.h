@@ -292,7 +292,8 @@ int pc_intpeak(int device, int kind, double *ops_per_s);
  * variant), "host_mode" (0..3 host pipeline), "ctas_per_sm", "dev_direct",
  * "peer_direct" (device-memory endpoints, see (v)), "svc_direct" (0/1/2 auto:
  * worker service doorbell polling), "run_desc" (1: descriptor arrays at
- * ChaCha8/12 walk contiguous page runs per slot), "svc_pages" (key service
+ * ChaCha8/12 walk contiguous page runs per slot; 2: the same runs with one
+ * warp per page and two blocks per thread, any round count), "svc_pages" (key service
  * batch limit, 0 auto), "svc_bell_ops" (1: a store service's ticket slots
  * ride in the doorbell line); pc_tune_get also reads "launches", the number
  * of kernels this library has launched. */

@@ -768,6 +768,160 @@ k_crypt_pages_run(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *
 }
 
 // ---------------------------------------------------------------------------
+// v5r2: v5r's page runs with ONE WARP per page slot and two blocks per thread
+// (lane l takes blocks l and l + 32).  With per-page descriptor arrays the
+// per-page seed work -- the round-1 quarter round of column 0 (vaddr_lo) and,
+// with a pid array, of column 2 -- is what separates v5r from the contiguous
+// loop (+16 ALU-pipe instructions per page-warp, profiles/r02_desc_opmix.txt);
+// here each thread pays it once for two blocks, and the descriptor pair loads
+// are per warp instead of per two warps.  No shared memory beyond the ring
+// and no shuffles (v6/v9 lost on MIO, profiles/r02_desc_experiments.txt).
+// 128-thread CTAs: 4 slots x 3 stages x 4 KiB = 48 KiB static ring.
+template <int ROUNDS, int DM>
+__global__ void __launch_bounds__(128, 4)
+k_crypt_pages_run2(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *in, uint4 *out, uint32_t n_pages,
+                   uint32_t run) {
+  constexpr bool VA = (DM & 1) != 0, PA = (DM & 2) != 0;
+  constexpr RotMul rm{};
+  constexpr int kStages = 3;
+  __shared__ uint4 ring[kStages][128 * 8]; // 16 KiB per stage
+  const uint32_t tid = threadIdx.x;
+  const uint32_t l = tid & 31;
+  const uint32_t sw = (l >> 1) & 3;
+  uint32_t page = (blockIdx.x * 4 + (tid >> 5)) * run; // run is even
+  const uint32_t end = min(n_pages, page + run);
+  if (page >= end) return;
+  // block l of the slot's page at chunk (w*64 + l)*4, block l+32 at +32*4 chunks
+  const uint32_t base0 = smem_u32(&ring[0][((tid >> 5) * 64 + l) * 4]);
+  constexpr uint32_t kStageBytes = 128 * 8 * 16;
+  constexpr uint32_t kHalf = 32 * 4 * 16;
+  const uint4 *src_ahead = in + static_cast<uint64_t>(page) * 256 + l * 4;
+  uint4 *dst = out + static_cast<uint64_t>(page) * 256 + l * 4;
+  uint32_t page_ahead = page;
+  auto issue = [&](int st) {
+    if (page_ahead < end) {
+      const uint32_t sdst = base0 + st * kStageBytes;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async16(sdst + 16 * (c ^ sw), src_ahead + c);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async16(sdst + kHalf + 16 * (c ^ sw), src_ahead + 128 + c);
+    }
+    cp_async_commit();
+    page_ahead += 1;
+    src_ahead += 256;
+  };
+  issue(0);
+  issue(1);
+  uint32_t k[8];
+  load_key(key, k);
+  const uint32_t bA = l, bB = l + 32;
+  uint32_t a3a = kSigma3, a3b = k[3], a3c = k[7], a3d = bA;
+  quarter_round<0>(a3a, a3b, a3c, a3d, rm);
+  uint32_t b3a = kSigma3, b3b = k[3], b3c = k[7], b3d = bB;
+  quarter_round<0>(b3a, b3b, b3c, b3d, rm);
+  uint32_t c1a = 0, c1b = 0, c1c = 0, c1d = 0, c2a = 0, c2b = 0, c2c = 0, c2d = 0;
+  uint32_t cached_hi = 0;
+  bool cached = false;
+  if constexpr (!PA) {
+    c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = desc.pid0;
+    quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+  }
+  auto load_pair = [&](uint32_t p, uint4 &vv, uint2 &pp) {
+    if (p + 1 < n_pages) {
+      if constexpr (VA) vv = __ldg(reinterpret_cast<const uint4 *>(desc.vaddrs + p));
+      if constexpr (PA) pp = __ldg(reinterpret_cast<const uint2 *>(desc.pids + p));
+    } else if (p < n_pages) {
+      if constexpr (VA) {
+        const uint64_t v = __ldg(desc.vaddrs + p);
+        vv = make_uint4(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32), 0, 0);
+      }
+      if constexpr (PA) pp = make_uint2(__ldg(desc.pids + p), 0);
+    }
+  };
+  uint4 vcur = make_uint4(0, 0, 0, 0), vnext = vcur;
+  uint2 pcur = make_uint2(0, 0), pnext = pcur;
+  load_pair(page, vcur, pcur);
+  load_pair(page + 2, vnext, pnext);
+  int st = 0;
+  // one page per iteration, not unrolled: two blocks of fully unrolled rounds
+  // are already twice v5's loop body (the i-cache)
+#pragma unroll 1
+  for (;;) {
+    const bool odd = (page & 1) != 0; // runs start on even pages
+    uint32_t vlo, vhi, pid;
+    if constexpr (VA) {
+      vlo = odd ? vcur.z : vcur.x;
+      vhi = odd ? vcur.w : vcur.y;
+    } else {
+      const uint64_t v = desc.vaddr0 + (static_cast<uint64_t>(page) << 12);
+      vlo = static_cast<uint32_t>(v);
+      vhi = static_cast<uint32_t>(v >> 32);
+    }
+    if constexpr (PA) pid = odd ? pcur.y : pcur.x;
+    else pid = desc.pid0;
+    if (odd) { // the pair is consumed: the next one is resident, fetch the one after
+      vcur = vnext;
+      pcur = pnext;
+      load_pair(page + 3, vnext, pnext);
+    }
+    issue(st == 0 ? 2 : st - 1); // stage (st + 2) % 3
+    if (!cached || vhi != cached_hi) {
+      c1a = kSigma1; c1b = k[1]; c1c = k[5]; c1d = vhi;
+      quarter_round<0>(c1a, c1b, c1c, c1d, rm);
+      cached_hi = vhi;
+      cached = true;
+    }
+    if constexpr (PA) {
+      c2a = kSigma2; c2b = k[2]; c2c = k[6]; c2d = pid;
+      quarter_round<0>(c2a, c2b, c2c, c2d, rm);
+    }
+    uint32_t c0a = kSigma0, c0b = k[0], c0c = k[4], c0d = vlo; // shared by both blocks
+    quarter_round<0>(c0a, c0b, c0c, c0d, rm);
+    uint32_t x[16], y[16];
+    x[0] = c0a; x[4] = c0b; x[8] = c0c; x[12] = c0d;
+    x[1] = c1a; x[5] = c1b; x[9] = c1c; x[13] = c1d;
+    x[2] = c2a; x[6] = c2b; x[10] = c2c; x[14] = c2d;
+    x[3] = a3a; x[7] = a3b; x[11] = a3c; x[15] = a3d;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) y[i] = x[i];
+    y[3] = b3a; y[7] = b3b; y[11] = b3c; y[15] = b3d;
+    diagonal_round<0>(x, rm);
+    diagonal_round<0>(y, rm);
+#pragma unroll
+    for (int r = 1; r < ROUNDS / 2; ++r) {
+      column_round<0>(x, rm);
+      column_round<0>(y, rm);
+      diagonal_round<0>(x, rm);
+      diagonal_round<0>(y, rm);
+    }
+    cp_async_wait<2>(); // this page's group has landed
+    const uint4 *mine = &ring[st][((tid >> 5) * 64 + l) * 4];
+    {
+      const uint4 d0 = mine[0 ^ sw], d1 = mine[1 ^ sw], d2 = mine[2 ^ sw], d3 = mine[3 ^ sw];
+      st_v8(dst, make_uint4(d0.x ^ (x[0] + kSigma0), d0.y ^ (x[1] + kSigma1), d0.z ^ (x[2] + kSigma2),
+                            d0.w ^ (x[3] + kSigma3)),
+            make_uint4(d1.x ^ (x[4] + k[0]), d1.y ^ (x[5] + k[1]), d1.z ^ (x[6] + k[2]), d1.w ^ (x[7] + k[3])));
+      st_v8(dst + 2, make_uint4(d2.x ^ (x[8] + k[4]), d2.y ^ (x[9] + k[5]), d2.z ^ (x[10] + k[6]), d2.w ^ (x[11] + k[7])),
+            make_uint4(d3.x ^ (x[12] + vlo), d3.y ^ (x[13] + vhi), d3.z ^ (x[14] + pid), d3.w ^ (x[15] + bA)));
+    }
+    {
+      const uint4 *m2 = mine + 128;
+      const uint4 d0 = m2[0 ^ sw], d1 = m2[1 ^ sw], d2 = m2[2 ^ sw], d3 = m2[3 ^ sw];
+      st_v8(dst + 128, make_uint4(d0.x ^ (y[0] + kSigma0), d0.y ^ (y[1] + kSigma1), d0.z ^ (y[2] + kSigma2),
+                                  d0.w ^ (y[3] + kSigma3)),
+            make_uint4(d1.x ^ (y[4] + k[0]), d1.y ^ (y[5] + k[1]), d1.z ^ (y[6] + k[2]), d1.w ^ (y[7] + k[3])));
+      st_v8(dst + 130, make_uint4(d2.x ^ (y[8] + k[4]), d2.y ^ (y[9] + k[5]), d2.z ^ (y[10] + k[6]), d2.w ^ (y[11] + k[7])),
+            make_uint4(d3.x ^ (y[12] + vlo), d3.y ^ (y[13] + vhi), d3.z ^ (y[14] + pid), d3.w ^ (y[15] + bB)));
+    }
+    page += 1;
+    if (page >= end) break;
+    dst += 256;
+    st = st == 2 ? 0 : st + 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // v6: v5's cp.async page ring with the per-page seed rounds computed once
 // per page instead of once per thread.
 //

@@ -247,7 +247,8 @@ cudaMemPool_t seed_pool(int dev) {
   return p;
 }
 
-template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async, 3 = v6 warp-shared seeds, 4 = v9 seeded
+template <int R, int Variant> // 0 = v2, 1 = v3 coalesced, 2 = v5 cp.async, 3 = v6 warp-shared seeds, 4 = v9 seeded,
+                              // 5 = v5r2 (128-thread CTAs: the grid is in CTAs of 4 warp slots)
 unsigned pages_grid(size_t n_pages) {
   static std::atomic<uint32_t> geo[64] = {};
   int dev = 0, n_sm = 0, occ = 0;
@@ -264,6 +265,8 @@ unsigned pages_grid(size_t n_pages) {
           if (e2 != cudaSuccess) return e2;
           return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_warp<R, 0>, 256, pc::kV6Smem);
         }
+        else if constexpr (Variant == 5)
+          return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pc::k_crypt_pages_run2<R, 3>, 128, 0);
         else if constexpr (Variant == 4) {
           cudaError_t e2 = v9_opt_in<R>();
           if (e2 != cudaSuccess) return e2;
@@ -304,10 +307,28 @@ void launch_pages_r(int kern, const uint32_t *key, const pc::PageDesc &d, const 
       const auto a = i4 + p0 * 256;
       const auto b = o4 + p0 * 256;
       const int dm = (dd.vaddrs ? 1 : 0) | (dd.pids ? 2 : 0);
+      const int rd = tuning().run_desc.load();
+      if (dm && rd == 2 &&
+          (reinterpret_cast<uintptr_t>(dd.vaddrs) & 15) == 0 && (reinterpret_cast<uintptr_t>(dd.pids) & 7) == 0) {
+        // one warp per page slot, two blocks per thread
+        const unsigned g2 = pages_grid<R, 5>(m);
+        if (g2) {
+          const uint64_t slots = uint64_t(g2) * 4;
+          const uint32_t run = static_cast<uint32_t>((((m + slots - 1) / slots) + 1) & ~uint64_t(1));
+          const unsigned g = static_cast<unsigned>((m + uint64_t(run) * 4 - 1) / (uint64_t(run) * 4));
+          switch (dm) {
+            case 1: pc::k_crypt_pages_run2<R, 1><<<g, 128, 0, st>>>(key, dd, a, b, m, run); break;
+            case 2: pc::k_crypt_pages_run2<R, 2><<<g, 128, 0, st>>>(key, dd, a, b, m, run); break;
+            default: pc::k_crypt_pages_run2<R, 3><<<g, 128, 0, st>>>(key, dd, a, b, m, run); break;
+          }
+          counted();
+          continue;
+        }
+      }
       if constexpr (R <= PC_RUN_MAX_R) {
         // descriptor arrays at ChaCha8/12: contiguous page runs per slot, so a
         // page pair's descriptors are one 16-byte and one 8-byte load
-        if (dm && tuning().run_desc.load() && grid &&
+        if (dm && rd && grid &&
             (reinterpret_cast<uintptr_t>(dd.vaddrs) & 15) == 0 && (reinterpret_cast<uintptr_t>(dd.pids) & 7) == 0) {
           const uint64_t slots = uint64_t(grid) * 4;
           const uint32_t run = static_cast<uint32_t>((((m + slots - 1) / slots) + 1) & ~uint64_t(1));
@@ -1752,6 +1773,9 @@ cudaError_t touch_rounds() {
     acc(touch(pc::k_crypt_pages_run<R, 2>));
     acc(touch(pc::k_crypt_pages_run<R, 3>));
   }
+  acc(touch(pc::k_crypt_pages_run2<R, 1>));
+  acc(touch(pc::k_crypt_pages_run2<R, 2>));
+  acc(touch(pc::k_crypt_pages_run2<R, 3>));
   acc(v6_opt_in<R, 0>()); // loads the module and sets the shared-memory opt-in
   acc(v6_opt_in<R, 1>());
   acc(v6_opt_in<R, 2>());
@@ -2327,7 +2351,7 @@ int pc_tune(const char *knob, int64_t value) {
     return PC_OK;
   }
   if (!std::strcmp(knob, "run_desc")) {
-    if (value != 0 && value != 1) return fail(PC_EINVAL, "run_desc must be 0 or 1");
+    if (value < 0 || value > 2) return fail(PC_EINVAL, "run_desc must be 0, 1 or 2");
     t.run_desc = static_cast<int>(value);
     return PC_OK;
   }

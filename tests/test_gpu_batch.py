@@ -89,7 +89,7 @@ class TestDevicePath:
     @pytest.mark.parametrize("rounds", [8, 12, 20])
     @pytest.mark.parametrize("n", [1, 2, 3, 5, 1183, 2369, 4097])
     @pytest.mark.parametrize("kernel", [0, 5, 6, 9])
-    @pytest.mark.parametrize("run_desc", [0, 1])
+    @pytest.mark.parametrize("run_desc", [0, 1, 2])
     def test_every_descriptor_shape_ragged(self, dkey, shape, rounds, n, kernel, run_desc, knob):
         """Each descriptor shape compiles to its own loop (DM = vaddr array |
         pid array; page-pair loops for R <= 12 and for R = 20 with a vaddr
@@ -117,7 +117,8 @@ class TestDevicePath:
 
     @pytest.mark.parametrize("rounds", [8, 12])
     @pytest.mark.parametrize("offset", [0, 1])
-    def test_run_desc_alignment_fallback(self, dkey, rounds, offset, knob):
+    @pytest.mark.parametrize("run_desc", [1, 2])
+    def test_run_desc_alignment_fallback(self, dkey, rounds, offset, run_desc, knob):
         """v5's page-run loop loads a page pair's descriptors as one 16-byte
         vaddr and one 8-byte pid load; arrays that start off that alignment
         (a tensor view one element in) take the per-page loop.  Both equal
@@ -125,7 +126,7 @@ class TestDevicePath:
         import torch
 
         knob("kernel", 5)
-        knob("run_desc", 1)
+        knob("run_desc", run_desc)  # 2: one warp per page slot, two blocks per thread
         for n in (1, 2, 7, 1184, 2371):
             rng = np.random.default_rng(n + offset)
             pages = rng.integers(0, 256, size=(n, 4096), dtype=np.uint8)
