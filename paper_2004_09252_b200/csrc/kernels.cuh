@@ -768,6 +768,9 @@ k_crypt_pages_run(const uint32_t *__restrict__ key, PageDesc desc, const uint4 *
 }
 
 // ---------------------------------------------------------------------------
+#ifndef PC_RUN2_R20_UNROLL
+#define PC_RUN2_R20_UNROLL 3
+#endif
 // v5r2: v5r's page runs with ONE WARP per page slot and two blocks per thread
 // (lane l takes blocks l and l + 32).  With per-page descriptor arrays the
 // per-page seed work -- the round-1 quarter round of column 0 (vaddr_lo) and,
@@ -887,7 +890,10 @@ k_crypt_pages_run2(const uint32_t *__restrict__ key, PageDesc desc, const uint4 
     y[3] = b3a; y[7] = b3b; y[11] = b3c; y[15] = b3d;
     diagonal_round<0>(x, rm);
     diagonal_round<0>(y, rm);
-#pragma unroll
+    // R = 20: three double rounds per loop trip (the fully unrolled pair of
+    // blocks is ~4200 SASS instructions and thrashes the i-cache)
+    constexpr int kUnroll = ROUNDS > 12 ? PC_RUN2_R20_UNROLL : ROUNDS / 2 - 1;
+#pragma unroll kUnroll
     for (int r = 1; r < ROUNDS / 2; ++r) {
       column_round<0>(x, rm);
       column_round<0>(y, rm);
