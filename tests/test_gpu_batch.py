@@ -115,6 +115,39 @@ class TestDevicePath:
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=rounds, nthreads=8))
 
+    @pytest.mark.parametrize("rounds", [8, 12, 20])
+    @pytest.mark.parametrize("run_desc", [0, 1, 2])
+    @pytest.mark.parametrize("n", [1, 2, 3, 593, 1186])
+    def test_descriptor_loops_stay_inside_the_batch(self, dkey, rounds, run_desc, n, knob):
+        """The batch is a window of a larger buffer with guard pages on both
+        sides and its descriptor arrays are windows of longer arrays: every
+        descriptor loop (v5 strided, page runs, two blocks per thread) writes
+        exactly the window and leaves the guards and the input untouched
+        (compute-sanitizer is not available on this pool; this is the write
+        side of its memcheck)."""
+        import torch
+
+        knob("kernel", 5)
+        knob("run_desc", run_desc)
+        g = 3  # guard pages each side
+        rng = np.random.default_rng(n * 7 + rounds + run_desc)
+        pages = rng.integers(0, 256, size=(n + 2 * g, 4096), dtype=np.uint8)
+        va = rng.integers(0, 2**52, size=n + 2 * g, dtype=np.uint64) << np.uint64(12)
+        pi = rng.integers(0, 2**32, size=n + 2 * g, dtype=np.uint64).astype(np.uint32)
+        src = t(pages)
+        dst = torch.full_like(src, 0xA5)
+        v_t = t(va.view(np.int64))[g:g + n]  # offset g = 3: 8-byte aligned only (v5 fallback) ...
+        p_t = t(pi.view(np.int32))[g:g + n]
+        for vv, pp, lo in ((v_t, p_t, g), (t(va[g:g + n].copy().view(np.int64)), t(pi[g:g + n].copy().view(np.int32)), g)):
+            dst.fill_(0xA5)  # ... and fresh, aligned copies (the run loops)
+            pc.crypt_pages(dkey, vv, pp, src[lo:lo + n], out=dst[lo:lo + n], rounds=rounds)
+            torch.cuda.synchronize()
+            got = dst.cpu().numpy()
+            assert (got[:lo] == 0xA5).all() and (got[lo + n:] == 0xA5).all()
+            want = C.crypt_pages(KEY, va[g:g + n], pi[g:g + n], pages[g:g + n], rounds=rounds)
+            assert np.array_equal(got[lo:lo + n], want)
+        assert np.array_equal(src.cpu().numpy(), pages)
+
     @pytest.mark.parametrize("rounds", [8, 12])
     @pytest.mark.parametrize("offset", [0, 1])
     @pytest.mark.parametrize("run_desc", [1, 2])

@@ -43,10 +43,15 @@ def main():
                 # every descriptor shape (vaddr array and/or pid array)
                 dva = torch.from_numpy(va.view(np.int64)).cuda()
                 dpi = torch.from_numpy(pi.view(np.int32)).cuda()
-                for v_arg, p_arg, v_ref, p_ref in ((dva, dpi, va, pi), (dva, 7, va, np.full(n, 7, np.uint32)),
-                                                   (0x5000, dpi, 0x5000 + 4096 * np.arange(n, dtype=np.uint64), pi)):
-                    got = pc.crypt_pages(k, v_arg, p_arg, torch.from_numpy(pages).cuda(), rounds=r)
-                    assert np.array_equal(got.cpu().numpy(), C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=r)), (kern, r)
+                # v5's descriptor loops: strided (run_desc 0), page runs (1), runs with two blocks per thread (2)
+                for rd in ((0, 1, 2) if kern == 5 else (1,)):
+                    _native.tune("run_desc", rd)
+                    for v_arg, p_arg, v_ref, p_ref in ((dva, dpi, va, pi), (dva, 7, va, np.full(n, 7, np.uint32)),
+                                                       (0x5000, dpi, 0x5000 + 4096 * np.arange(n, dtype=np.uint64), pi)):
+                        got = pc.crypt_pages(k, v_arg, p_arg, torch.from_numpy(pages).cuda(), rounds=r)
+                        want = C.crypt_pages(KEY, v_ref, p_ref, pages, rounds=r)
+                        assert np.array_equal(got.cpu().numpy(), want), (kern, r, rd)
+                _native.tune("run_desc", 1)
         _native.tune("kernel", 0)
         print("host paths", flush=True)
         for hm in (0, 1, 2, 3):
