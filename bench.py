@@ -639,6 +639,7 @@ def split_parity(pc, key, torch, dist, world, rank, dev, backend, g_pages: int =
     no collective.)"""
     from paper_2004_09252_b200.partition import shard
 
+    g_pages -= g_pages % world  # equal ranges for all_gather at any N
     gen = torch.Generator(device=dev).manual_seed(4242)
     batch = torch.randint(0, 256, (g_pages, PAGE), dtype=torch.uint8, device=dev, generator=gen)
     lo, hi = shard(g_pages, rank, world)
@@ -647,7 +648,7 @@ def split_parity(pc, key, torch, dist, world, rank, dev, backend, g_pages: int =
     torch.cuda.synchronize()
     if world > 1:
         t = mine if backend == "nccl" else mine.cpu()
-        parts = [torch.empty_like(t) for _ in range(world)]  # g_pages % world == 0 for N in 1,2,4,8
+        parts = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(parts, t)
         got = torch.cat([p.to(dev) for p in parts])
     else:
@@ -678,7 +679,9 @@ def sweep_leg(pc, key, torch, args, rank, world, dev, barrier, max_over_ranks, r
     vaddr0 = BASE_VADDR + PAGE * lo
     res = {"gib_total": args.sweep_gib, "pages_total": total_pages, "pages_per_rank": m, "ranks": world}
     free_b, _ = torch.cuda.mem_get_info(dev)
-    if m * PAGE > free_b - (4 << 30):
+    # every branch below that skips is decided over all ranks (the timed
+    # paths hold barriers and reductions: one rank skipping alone would hang)
+    if max_over_ranks(float(m * PAGE > free_b - (4 << 30)), device=red_dev) > 0:
         res["device"] = {"skipped": f"share {m * PAGE / 2**30:.1f} GiB does not fit ({free_b / 2**30:.1f} GiB free)"}
     else:
         buf = torch.empty((m, PAGE), dtype=torch.uint8, device=dev)
@@ -704,14 +707,19 @@ def sweep_leg(pc, key, torch, args, rank, world, dev, barrier, max_over_ranks, r
         del buf, probe
         torch.cuda.empty_cache()
     avail = _mem_available()
-    if avail is not None and m * PAGE * world > 0.6 * avail:
+    too_big = avail is not None and m * PAGE * world > 0.6 * avail
+    if max_over_ranks(float(too_big), device=red_dev) > 0:
         res["host"] = {"skipped": f"{m * PAGE * world / 2**30:.0f} GiB pinned over all ranks exceeds 60% of "
                                   f"MemAvailable ({avail / 2**30:.0f} GiB)"}
         return res
+    host, err = None, None
     try:
         host = torch.empty((m, PAGE), dtype=torch.uint8).pin_memory()
     except RuntimeError as exc:
-        res["host"] = {"skipped": f"pinned {m * PAGE / 2**30:.1f} GiB failed: {exc}"[:200]}
+        err = f"pinned {m * PAGE / 2**30:.1f} GiB failed: {exc}"[:200]
+    if max_over_ranks(float(err is not None), device=red_dev) > 0:
+        del host
+        res["host"] = {"skipped": err or "pinning failed on another rank"}
         return res
     host[::64].random_(0, 256)
     probe = host[::64].clone()
