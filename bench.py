@@ -77,6 +77,7 @@ class ClockSampler:
         self.samples: list[tuple[float, float, float, int]] = []
         self._stop = threading.Event()
         self._nvml = None
+        self.pci = None
 
     def __enter__(self):
         try:
@@ -84,7 +85,18 @@ class ClockSampler:
 
             pynvml.nvmlInit()
             self._nvml = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._h = None
+            try:  # the CUDA device's own PCI address: NVML indices ignore CUDA_VISIBLE_DEVICES
+                import torch
+
+                p = torch.cuda.get_device_properties(self.gpu)
+                bdf = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bdf)
+                self.pci = bdf
+            except Exception:
+                pass
+            if self._h is None:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
@@ -116,7 +128,8 @@ class ClockSampler:
         reasons = sorted({name for _, _, _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": float(self.max_mhz),
                 "reasons": reasons, "power_w_max": round(max(x[2] for x in self.samples), 1),
-                "samples": len(sm), "source": "NVML every %g ms during the timed region" % (1e3 * self.period)}
+                "samples": len(sm), "source": "NVML every %g ms during the timed region" % (1e3 * self.period),
+                "nvml_device": self.pci or f"index {self.gpu}"}
 
 
 # ---------------------------------------------------------------------------
