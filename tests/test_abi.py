@@ -117,3 +117,28 @@ def test_header_is_plain_c_and_links(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert "NULL" in r.stdout
+
+
+@pytest.mark.parametrize("knob,good,bad", [
+    ("run_desc", [0, 1, 2], [-1, 3]),
+    ("kernel", [0, 1, 2, 3, 4, 5, 6, 9], [-1, 7, 8, 10]),
+    ("svc_pages", [0, 1, 64], [-1, 65]),
+    ("small_mode", [0, 1], [2]),
+])
+def test_tuning_knobs_validate_without_a_gpu(knob, good, bad):
+    """pc_tune range-checks every knob value (no device is touched); a bad
+    value leaves the knob as it was."""
+    before = _native.tune_get(knob)
+    try:
+        for v in good:
+            _native.tune(knob, v)
+            assert _native.tune_get(knob) == v
+        _native.tune(knob, good[0])
+        for v in bad:
+            with pytest.raises(ContractViolation):
+                _native.tune(knob, v)
+            assert _native.tune_get(knob) == good[0]
+    finally:
+        _native.tune(knob, before)
+    with pytest.raises(ContractViolation):
+        _native.tune("no_such_knob", 1)
