@@ -529,6 +529,29 @@ bool pinned_alias(const void *p, void **dev) {
   return true;
 }
 
+// Both answers from ONE cudaPointerGetAttributes (the fault-sized path asks
+// for each of its two buffers; every query is a driver call).
+struct PtrInfo {
+  bool dev = false;        // device (or managed) memory of GPU `device`
+  int device = -1;
+  void *host_dev = nullptr; // pinned host memory: its device-visible alias
+};
+PtrInfo ptr_info(const void *p) {
+  PtrInfo r;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return r;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    r.dev = true;
+    r.device = a.device;
+  } else if (a.type == cudaMemoryTypeHost) {
+    r.host_dev = a.devicePointer;
+  }
+  return r;
+}
+
 // Is p device memory (of any GPU; managed memory counts)?  *device = its GPU.
 bool device_memory(const void *p, int *device) {
   cudaPointerAttributes a;
@@ -1198,7 +1221,7 @@ namespace {
 // no copies); copy mode does one H2D, the kernel and one D2H.
 int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, const uint64_t *vaddrs,
                 const uint32_t *pids, uint64_t vaddr0, uint32_t pid0, const void *in, void *out,
-                size_t n, int rounds) {
+                size_t n, int rounds, void *in_dev, void *out_dev) {
   const size_t off_v = 256, off_p = off_v + ((n * 8 + 255) & ~size_t(255));
   const size_t off_pg = off_p + ((n * 4 + 255) & ~size_t(255));
   const size_t used = off_pg + n * PC_PAGE_SIZE;
@@ -1206,8 +1229,8 @@ int crypt_small(pc_engine *e, const uint32_t *dkey, const uint8_t *raw_key, cons
   cudaStream_t st = e->streams[0];
   const bool zc = tuning().small_mode == 1;
   // zero-copy straight on the caller's pages when they are pinned already
-  void *in_dev = nullptr, *out_dev = nullptr;
-  const bool direct = zc && pinned_alias(in, &in_dev) && pinned_alias(out, &out_dev);
+  // (in_dev/out_dev: their device aliases, from the caller's pointer query)
+  const bool direct = zc && in_dev && out_dev;
   if (raw_key) std::memcpy(h, raw_key, 32);
   if (vaddrs) std::memcpy(h + off_v, vaddrs, n * 8);
   if (pids) std::memcpy(h + off_p, pids, n * 4);
@@ -1439,18 +1462,20 @@ int pc_crypt_pages_host(pc_engine *e, const pc_key *key, const uint8_t *raw_key,
     // (profiles/r02_key_service_sweep.json)
     const size_t max_pages = std::min<size_t>(
         kSvcMaxPages, lim > 0 ? static_cast<size_t>(lim) : std::min<size_t>(6, static_cast<size_t>(key->svc_workers)));
-    int gin = -1, gout = -1;
-    if (key->svc && key->svc_rounds == rounds && n <= max_pages && !device_memory(in, &gin) &&
-        !device_memory(out, &gout))
-      return crypt_on_service(key, vaddrs, pids, vaddr0, pid0, in, out, n);
+    if (key->svc && key->svc_rounds == rounds && n <= max_pages) {
+      const PtrInfo a = ptr_info(in), b = ptr_info(out);
+      if (!a.dev && !b.dev) return crypt_on_service(key, vaddrs, pids, vaddr0, pid0, in, out, n);
+    }
   }
   std::lock_guard<std::mutex> lk(e->mu);
   DeviceGuard g(e->device);
   CU(g.err);
-  int gin = -1, gout = -1;
-  const bool din = device_memory(in, &gin), dout = device_memory(out, &gout);
+  const PtrInfo pin = ptr_info(in), pout = ptr_info(out);
+  const bool din = pin.dev, dout = pout.dev;
+  const int gin = pin.device, gout = pout.device;
   if (n <= tuning().small_max && !din && !dout)
-    return crypt_small(e, raw_key ? nullptr : key->d_words, raw_key, vaddrs, pids, vaddr0, pid0, in, out, n, rounds);
+    return crypt_small(e, raw_key ? nullptr : key->d_words, raw_key, vaddrs, pids, vaddr0, pid0, in, out, n, rounds,
+                       pin.host_dev, pout.host_dev);
   if (din && dout && gin == e->device && gout == e->device && !vaddrs && !pids && !raw_key &&
       tuning().dev_direct.load()) {
     // pages already in this GPU's memory: one in-place launch, no staging
